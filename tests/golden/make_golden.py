@@ -1,0 +1,212 @@
+"""Generate golden vectors by running the REFERENCE package (cpfit) itself.
+
+Run here, in the build container, where /root/reference exists:
+
+    python tests/golden/make_golden.py
+
+It imports ``cpfit`` read-only from /root/reference/pkg/src (numba JIT on,
+cache in /tmp), builds seeded inputs, runs the reference's own public API and
+writes compressed ``.npz`` fixtures next to this script.  The fixtures travel
+to the GPU box; /root/reference does not, so nothing else reads it at run time.
+
+Fixtures:
+  kernels_small.npz  -- 120 random small cases (order 2-4, dims <= 6, R <= 4):
+                        tttp (with absent factors), mttkrp, gram_blocks,
+                        solve_factor, counting_sort_by_mode
+  layout.npz         -- from_coords with duplicates, counting sort perms of a
+                        20k-entry tensor, linearize/delinearize round trip
+  philox.npz         -- RngState draws and SparseTensor.sample keep-sets
+  cfg1.npz           -- BASELINE cfg 1: tttp, mttkrp x3, 5 ALS sweeps (+rmse),
+                        2 CCD++ sweeps, 3 SGD steps, all from the reference
+  drivers_small.npz  -- ALS/CCD/SGD single sweeps and run() traces, small case
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_golden")
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import cpfit  # noqa: E402  (the reference)
+from cpfit import kernels as rk  # noqa: E402
+from cpfit import optim as ro  # noqa: E402
+
+from paper_1910_02371_b200 import synth  # noqa: E402
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def random_sparse(shape, density, rng, ensure_nonempty=True):
+    total = int(np.prod(shape))
+    mask = rng.random(total) < density
+    if ensure_nonempty and not mask.any():
+        mask[rng.integers(0, total)] = True
+    keys = np.flatnonzero(mask).astype(np.uint64)
+    values = rng.standard_normal(keys.size)
+    return cpfit.SparseTensor(shape, keys, values)
+
+
+def kernels_small():
+    rng = np.random.default_rng(20240)
+    out = {}
+    n_cases = 120
+    for c in range(n_cases):
+        order = int(rng.integers(2, 5))
+        dims = tuple(int(d) for d in rng.integers(1, 7, order))
+        rank = int(rng.integers(1, 5))
+        t = random_sparse(dims, 0.45, rng, ensure_nonempty=(c % 7 != 0))
+        factors = [rng.standard_normal((d, rank)) for d in dims]
+        mode = int(rng.integers(0, order))
+        absent = -1
+        if order > 2 and rng.random() < 0.4:
+            absent = int(rng.integers(0, order))
+        tf = list(factors)
+        if absent >= 0:
+            tf[absent] = None
+        weights = t.with_values(np.abs(t.values) + 0.1)
+        rhs = rng.standard_normal((dims[mode], rank))
+        reg = float(rng.random() * 0.5 + 0.1)
+        p = f"c{c}_"
+        out[p + "dims"] = np.array(dims, dtype=np.int64)
+        out[p + "keys"] = t.keys
+        out[p + "values"] = t.values
+        out[p + "mode"] = np.array(mode)
+        out[p + "absent"] = np.array(absent)
+        out[p + "reg"] = np.array(reg)
+        out[p + "rhs"] = rhs
+        for n, f in enumerate(factors):
+            out[p + f"f{n}"] = f
+        out[p + "tttp"] = rk.tttp(t, tf).values
+        out[p + "mttkrp"] = rk.mttkrp(t, factors, mode)
+        out[p + "gram"] = rk.gram_blocks(weights, factors, mode)
+        out[p + "solve"] = rk.solve_factor(weights, factors, rhs, mode, reg=reg)
+        perm, offsets = cpfit.counting_sort_by_mode(t, mode)
+        out[p + "perm"] = perm
+        out[p + "offsets"] = offsets
+    out["n_cases"] = np.array(n_cases)
+    np.savez_compressed(os.path.join(HERE, "kernels_small.npz"), **out)
+
+
+def layout():
+    rng = np.random.default_rng(77)
+    out = {}
+    dims = (7, 3, 9, 2)
+    coords = [rng.integers(0, d, 300) for d in dims]
+    vals = rng.standard_normal(300)
+    t = cpfit.from_coords(coords, vals, dims)
+    out["fc_dims"] = np.array(dims, dtype=np.int64)
+    out["fc_coords"] = np.stack(coords).astype(np.int64)
+    out["fc_values_in"] = vals
+    out["fc_keys"] = t.keys
+    out["fc_values"] = t.values
+    dims2 = (50, 40, 30)
+    t2 = random_sparse(dims2, 20_000 / 60_000, rng)
+    out["cs_dims"] = np.array(dims2, dtype=np.int64)
+    out["cs_keys"] = t2.keys
+    for mode in range(3):
+        perm, offsets = cpfit.counting_sort_by_mode(t2, mode)
+        out[f"cs_perm{mode}"] = perm
+        out[f"cs_offsets{mode}"] = offsets
+    dims3 = (480_189, 17_770, 2_182)
+    keys3 = np.sort(rng.integers(0, int(np.prod(np.array(dims3, dtype=object))), 5000,
+                                 dtype=np.uint64))
+    out["dl_dims"] = np.array(dims3, dtype=np.int64)
+    out["dl_keys"] = keys3
+    out["dl_coords"] = np.stack(cpfit.delinearize_many(keys3, dims3))
+    np.savez_compressed(os.path.join(HERE, "layout.npz"), **out)
+
+
+def philox():
+    out = {}
+    cases = [(0, ()), (42, (1,)), (123, (1, 7)), (5, (1, 3)), (2**40 + 3, (0,))]
+    for i, (seed, path) in enumerate(cases):
+        g = cpfit.RngState(seed, path).generator()
+        out[f"u{i}_seed"] = np.array(seed, dtype=np.uint64)
+        out[f"u{i}_path"] = np.array(path, dtype=np.int64)
+        draws = g.random(100_003)
+        out[f"u{i}_head"] = draws[:257]
+        out[f"u{i}_tail"] = draws[-37:]
+        out[f"u{i}_sum"] = np.array(draws.sum())
+    keys = np.arange(10_000, dtype=np.uint64) * np.uint64(3)
+    t = cpfit.SparseTensor((40_000,), keys, np.arange(10_000, dtype=np.float64))
+    for j, (rate, seed, path) in enumerate([(0.01, 3, (1, 1)), (0.1, 3, (1, 2)),
+                                            (0.5, 9, (1, 5)), (1.0, 1, ())]):
+        s = t.sample(rate, cpfit.RngState(seed, path))
+        out[f"s{j}_rate"] = np.array(rate)
+        out[f"s{j}_seed"] = np.array(seed)
+        out[f"s{j}_path"] = np.array(path, dtype=np.int64)
+        out[f"s{j}_keys"] = s.keys
+    out["n_uniform"] = np.array(len(cases))
+    out["n_sample"] = np.array(4)
+    np.savez_compressed(os.path.join(HERE, "philox.npz"), **out)
+
+
+def cfg1():
+    shape, keys, values, factors = synth.cfg1()
+    t = cpfit.SparseTensor(shape, keys, values)
+    out = {"keys_sha": np.array(sha(keys)), "values_sha": np.array(sha(values)),
+           "factors_sha": np.array(sha(np.concatenate([f.ravel() for f in factors])))}
+    out["tttp"] = rk.tttp(t, factors).values
+    for mode in range(3):
+        out[f"mttkrp{mode}"] = rk.mttkrp(t, factors, mode)
+    loss = cpfit.get_loss("ls")
+    cfg = ro.SolverConfig(rank=10, reg=1e-5)
+    state = ro.CompletionState(factors=[f.copy() for f in factors], rng=cpfit.RngState(0))
+    for s in range(5):
+        ro.als_sweep(t, state, loss, cfg)
+        for n in range(3):
+            out[f"als{s}_f{n}"] = state.factors[n].copy()
+        out[f"als{s}_rmse"] = np.array(cpfit.rmse(t, state.factors))
+    out["als_gram2"] = state.ls_gram[2][:5].copy()
+    out["als_rhs2"] = state.ls_rhs[2].copy()
+    state = ro.CompletionState(factors=[f.copy() for f in factors], rng=cpfit.RngState(0))
+    for s in range(2):
+        ro.ccd_sweep(t, state, loss, cfg)
+        for n in range(3):
+            out[f"ccd{s}_f{n}"] = state.factors[n].copy()
+    scfg = ro.SolverConfig(rank=10, reg=1e-4, step=1e-3, sample_rate=0.1,
+                           algorithm="sgd")
+    state = ro.CompletionState(factors=[f.copy() for f in factors], rng=cpfit.RngState(0))
+    for it in range(1, 4):
+        ro.sgd_sweep(t, state, loss, scfg, cpfit.RngState(11).child(1).child(it))
+        for n in range(3):
+            out[f"sgd{it}_f{n}"] = state.factors[n].copy()
+    np.savez_compressed(os.path.join(HERE, "cfg1.npz"), **out)
+
+
+def drivers_small():
+    rng = np.random.default_rng(26)
+    t = random_sparse((8, 7, 6), 0.5, rng)
+    out = {"dims": np.array(t.shape), "keys": t.keys, "values": t.values}
+    for algo in ("als", "ccd", "sgd"):
+        cfg = ro.SolverConfig(rank=3, algorithm=algo, max_iters=4, seed=4,
+                              deterministic=True, sample_rate=0.5, step=1e-3,
+                              record_every=1)
+        trace, state = ro.run(t, cfg, return_state=True)
+        out[f"{algo}_obj"] = np.array([r.objective for r in trace.records])
+        out[f"{algo}_metric"] = np.array([r.metric for r in trace.records])
+        out[f"{algo}_iters"] = np.array([r.iteration for r in trace.records])
+        for n in range(3):
+            out[f"{algo}_f{n}"] = state.factors[n]
+    np.savez_compressed(os.path.join(HERE, "drivers_small.npz"), **out)
+
+
+if __name__ == "__main__":
+    kernels_small()
+    layout()
+    philox()
+    cfg1()
+    drivers_small()
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
