@@ -1,0 +1,390 @@
+"""Benchmark of the TTTP + sparse-MTTKRP hot path (BASELINE.json metric).
+
+Workload (BASELINE cfg 2, the configuration the metric is quoted on): sparse
+order-3 fp64 tensor 10,000^3 with 1e7 uniform distinct nonzeros, values
+N(0,1), int32 indices, R = 16 factors N(0, 1/R).  One *step* = one TTTP plus
+one sparse MTTKRP on each of the three modes.  ``value`` = nonzeros processed
+per second per kernel pass, i.e. 4 * nnz / step time, with inputs resident in
+HBM (device-resident factors/values, pattern built once = the reference's
+cached coords / mode groups).  ``e2e`` = the same metric through the public
+drop-in API with host (numpy, pinned) values and factors, host<->device copies
+inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (launched by torchrun, one rank per GPU, NCCL): weak scaling -- every
+rank owns a distinct 1e7-nonzero shard of one N x 1e7-nonzero tensor over the
+same index space; TTTP is local, the per-mode MTTKRP partial outputs (I_n x R)
+are summed with an NCCL all-reduce (the real exchange step of a
+nonzero-partitioned MTTKRP).  Time = max over ranks of device time.
+
+``--impl reference`` times the reference's CPU algorithm (the C restatement
+in oracle/, OpenMP over all host threads, restating the numba prange loops of
+_jit.py) on the same workload, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+R = 16
+NNZ = 10_000_000
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+REASON_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.marks = []
+
+    def start(self):
+        cmd = ["nvidia-smi", f"--id={self.index}",
+               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu",
+               "--format=csv,noheader,nounits", "-lms", "50"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, tag):
+        self.marks.append((tag, time.perf_counter()))
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        t0 = dict(self.marks).get("start", 0.0)
+        t1 = dict(self.marks).get("stop", time.perf_counter())
+        sm, mx, reasons, util = [], [], 0, []
+        window = [l for (t, l) in self.lines if t0 - 0.06 <= t <= t1 + 0.06] or \
+            [l for (_, l) in self.lines]
+        for l in window:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                r = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
+                u = float(parts[3])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx.append(m)
+            util.append(u)
+            reasons |= r
+        names = [n for b, n in REASON_BITS.items() if reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": names, "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+
+def algorithmic_bytes(order, nnz, rank, dims, vbytes=8, ibytes=4):
+    """gather-inclusive bytes per launch."""
+    tttp = nnz * (order * ibytes + 2 * vbytes + order * rank * vbytes)
+    mtt = [nnz * (order * ibytes + vbytes + (order - 1) * rank * vbytes) + dims[n] * rank * vbytes
+           for n in range(order)]
+    compulsory = nnz * (order * ibytes + 2 * vbytes) + sum(dims) * rank * vbytes
+    return tttp, mtt, compulsory
+
+
+def run_reference(args):
+    """CPU arm: the reference algorithm (oracle C restatement), all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_1910_02371_b200 import synth
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    shape, keys, values, factors = synth.cfg2()
+    t = O.OTensor(shape, keys, values)
+    for mode in range(3):  # warm caches like the reference's cached coords/groups
+        t.mode_group(mode)
+
+    def step():
+        O.tttp(t, factors)
+        for mode in range(3):
+            O.mttkrp(t, factors, mode)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = 4 * t.nnz / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE cfg 2 shape)",
+        "config": CONFIG,
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "port",
+                         "sample": f"full cfg 2 workload, {args.steps} steps after "
+                                   f"{args.warmup} warm-up (oracle/cpfit_oracle.c, OpenMP)"},
+        "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "nonzeros/sec for TTTP & MTTKRP (TTTP + MTTKRP all modes, per kernel pass)"
+CONFIG = {"workload": "BASELINE cfg 2: sparse 10000^3, 1e7 uniform distinct nnz, R=16, fp64; "
+                      "step = TTTP + MTTKRP modes 0,1,2",
+          "nnz_per_gpu": NNZ, "rank": R, "shape": [10000, 10000, 10000],
+          "l2": "inputs larger than L2 (0.28 GB index+value stream per pass > 126 MB); "
+                "factors (3.84 MB) L2-resident by design"}
+
+
+def cpu_baseline_sample(seconds=12.0):
+    from oracle import oracle as O
+    from paper_1910_02371_b200 import synth
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    shape, keys, values, factors = synth.cfg2()
+    t = O.OTensor(shape, keys, values)
+    for mode in range(3):
+        t.mode_group(mode)
+    O.tttp(t, factors)
+    O.mttkrp(t, factors, 0)  # warm
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        O.tttp(t, factors)
+        for mode in range(3):
+            O.mttkrp(t, factors, mode)
+        n += 1
+        if time.perf_counter() - t0 > seconds or n >= 50:
+            break
+    dt = (time.perf_counter() - t0) / n
+    return {"value": 4 * t.nnz / dt, "unit": "nnz/s", "cores": threads, "kind": "port",
+            "sample": f"{n} full cfg-2 steps (TTTP + 3 MTTKRP, 1e7 nnz) with "
+                      "oracle/cpfit_oracle.c on all host threads"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1910_02371_b200 as cp
+    from paper_1910_02371_b200 import _lib, synth
+    from paper_1910_02371_b200.core import _dtype_code
+
+    shape, keys, values, factors = synth.cfg2(seed=synth.CFG2_SEED + 1000 * rank)
+    if world > 1:
+        # factors are replicated: every rank uses rank 0's draw
+        factors = synth.cfg2(seed=synth.CFG2_SEED, nnz=16)[3]
+    t = cp.SparseTensor(shape, keys, values, validate=False)
+    dev = torch.device("cuda", local)
+    dfs = [torch.from_numpy(f).to(dev) for f in factors]
+    L = _lib.load()
+    pat = t.device_pattern()
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    vals = t.device_values(torch.float64)
+    svals = [t.sorted_values(m, torch.float64) for m in range(3)]
+    fptrs = _lib.ptr_array([f.data_ptr() for f in dfs])
+    tout = torch.empty(t.nnz, dtype=torch.float64, device=dev)
+    mouts = [torch.empty((shape[m], R), dtype=torch.float64, device=dev) for m in range(3)]
+    launches_per_step = 1
+    for m in range(3):
+        nt, ns, nsl = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(L.cpfit_pattern_mode_stats(pat.handle, m, sp, ctypes.byref(nt),
+                                              ctypes.byref(ns), ctypes.byref(nsl)))
+        launches_per_step += 1 + (1 if ns.value > 0 else 0)
+    F64 = _dtype_code(torch.float64)
+    ev = {k: [] for k in ("tttp", "m0", "m1", "m2")}
+
+    def step(record=False):
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        _lib.check(L.cpfit_tttp(pat.handle, F64, R, ctypes.c_void_p(vals.data_ptr()), fptrs,
+                                ctypes.c_void_p(tout.data_ptr()), sp))
+        if record:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+            ev["tttp"].append((e0, e1))
+        for m in range(3):
+            if record:
+                a = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            _lib.check(L.cpfit_mttkrp(pat.handle, m, F64, R,
+                                      ctypes.c_void_p(svals[m].data_ptr()), 1, fptrs,
+                                      ctypes.c_void_p(mouts[m].data_ptr()), sp))
+            if record:
+                b = torch.cuda.Event(enable_timing=True)
+                b.record(stream)
+                ev[f"m{m}"].append((a, b))
+            if world > 1:
+                dist.all_reduce(mouts[m])
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    clocks.mark("start")
+    start.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    stop.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark("stop")
+    ms = start.elapsed_time(stop)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+    clk = clocks.stop()
+    ms_step = ms / args.steps
+    value = world * 4 * t.nnz / (ms_step * 1e-3)
+
+    # per-kernel device time (CUDA events on the launching stream)
+    kt = {k: float(np.mean([a.elapsed_time(b) for a, b in v])) for k, v in ev.items()}
+    tb, mb, compulsory = algorithmic_bytes(3, t.nnz, R, shape)
+    peak, peak_kind = peaks()
+    kernels = {
+        "tttp": {"ms": kt["tttp"], "alg_bytes": tb, "gbs": tb / (kt["tttp"] * 1e-3) / 1e9},
+    }
+    for m in range(3):
+        kernels[f"mttkrp{m}"] = {"ms": kt[f"m{m}"], "alg_bytes": mb[m],
+                                 "gbs": mb[m] / (kt[f"m{m}"] * 1e-3) / 1e9}
+    for k in kernels.values():
+        k["frac"] = k["gbs"] / peak
+        k["nnz_per_s"] = t.nnz / (k["ms"] * 1e-3)
+    dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"], "peak": peak,
+                "unit": "GB/s", "frac": kernels[dom]["gbs"] / peak, "peak_kind": peak_kind,
+                "traffic": None,
+                "byte_model": "gather-inclusive algorithmic bytes, SURVEY.md 8(d)"}
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            roofline["traffic"] = json.load(open(tf)).get(dom)
+        except Exception:
+            pass
+
+    # e2e through the public API with pinned host buffers (rank-local)
+    e2e = None
+    if args.e2e_steps > 0:
+        pv = torch.from_numpy(values).pin_memory()
+        pf = [torch.from_numpy(f).pin_memory() for f in factors]
+        hv = pv.numpy()
+        hf = [p.numpy() for p in pf]
+
+        def api_step():
+            tv = t.with_values(hv)
+            out = cp.tttp(tv, hf)
+            _ = out.values
+            ms_ = [cp.mttkrp(tv, hf, m) for m in range(3)]
+            return out, ms_
+        api_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            api_step()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.e2e_steps
+        h2d = values.nbytes + 3 * factors[0].nbytes + 3 * 2 * factors[0].nbytes
+        d2h = t.nnz * 8 + sum(shape[m] * R * 8 for m in range(3))
+        e2e = {"value": world * 4 * t.nnz / dt, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
+               "path": "paper_1910_02371_b200.tttp/mttkrp with numpy (pinned) values and "
+                       "factors; values re-uploaded and re-permuted every step"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE cfg 2 shape/value laws)",
+            "config": dict(CONFIG, parallelism=f"nnz-shard{world}" if world > 1 else "1gpu"),
+            "roofline": roofline, "kernels": kernels,
+            "compulsory_bytes_per_pass": compulsory,
+            "clocks": clk, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_sample()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

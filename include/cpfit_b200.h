@@ -1,0 +1,141 @@
+/*
+ * cpfit_b200.h -- C-ABI of the B200-native sparse CP-completion kernels.
+ *
+ * Drop-in boundary for the hot path of the reference package `cpfit`
+ * (/root/reference/pkg/src/cpfit).  The reference has no native code; its
+ * only compiled seam is the numba pair in _jit.py, called from kernels.py:
+ *
+ *   _jit.tttp3(vals, i0, i1, i2, f0, f1, f2, out)         (_jit.py:49-59,
+ *                                                          kernels.py:123-128)
+ *   _jit.mttkrp3(sorted_vals, idx_a, idx_b, starts, rows,  (_jit.py:35-47,
+ *                fac_a, fac_b, out)                        kernels.py:66-74)
+ *
+ * plus the numpy/BLAS/LAPACK bodies of kernels.gram_blocks / solve_factor
+ * (kernels.py:159-267), the layout caches of SparseTensor (coords(),
+ * mode_group(), counting_sort_by_mode: core.py:141-157, 234-249) and
+ * SparseTensor.sample (core.py:173-183).  Each entry point below names the
+ * reference interface it replaces.
+ *
+ * Conventions: plain pointers and sizes only.  "device" pointers are CUDA
+ * global-memory pointers on the current device; `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  Factor matrices are row-major I_n x R,
+ * contiguous.  Arrays of per-mode pointers are host arrays of device pointers.
+ * Every function returns CPFIT_OK (0) or an error code; cpfit_last_error()
+ * gives the message of the last failure on the calling thread.  Results are
+ * deterministic run to run: no floating-point atomics anywhere.
+ */
+#ifndef CPFIT_B200_H
+#define CPFIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (the Python shim maps them onto the reference's exceptions) */
+#define CPFIT_OK 0
+#define CPFIT_EINVAL 1      /* ValueError: shapes, ranks, modes, ranges        */
+#define CPFIT_ECUDA 2       /* CUDA runtime / launch failure                   */
+#define CPFIT_ESINGULAR 3   /* NumericalError "mode m row i: singular ..."     */
+#define CPFIT_EEMPTYROW 4   /* NumericalError "mode m row i: no incident ..."  */
+#define CPFIT_ENEGWEIGHT 5  /* ValueError: negative normal-equation weights    */
+#define CPFIT_ENONFINITE 6  /* non-finite values where finiteness is required  */
+#define CPFIT_ENOMEM 7      /* device allocation failed                        */
+
+/* value dtypes */
+#define CPFIT_F64 0
+#define CPFIT_F32 1
+
+typedef struct cpfit_pattern cpfit_pattern; /* device-resident sparsity pattern */
+
+const char *cpfit_version(void);
+const char *cpfit_last_error(void);
+
+/* ---- pattern (layout) ------------------------------------------------- */
+
+/* Build a device pattern from sorted linearized keys (device uint64[nnz]).
+ * Delinearizes on the device into int32 per-mode coordinates.
+ * Replaces: SparseTensor.coords / delinearize_many (core.py:93-102,141-145). */
+int cpfit_pattern_create(int order, const int64_t *dims, int64_t nnz,
+                         const uint64_t *keys, void *stream,
+                         cpfit_pattern **out);
+
+/* Build a pattern from per-mode int32 coordinates already on the device and
+ * already in canonical (key) order; the arrays are copied. */
+int cpfit_pattern_create_coords(int order, const int64_t *dims, int64_t nnz,
+                                const int32_t *const *coords, void *stream,
+                                cpfit_pattern **out);
+
+int cpfit_pattern_destroy(cpfit_pattern *p);
+
+int cpfit_pattern_info(const cpfit_pattern *p, int *order, int64_t *nnz);
+
+/* Device pointer to the int32 coordinates of `mode` (canonical order). */
+int cpfit_pattern_coords(const cpfit_pattern *p, int mode,
+                         const int32_t **coords);
+
+/* Entries per work task of the segmented kernels (default 1024).  Long
+ * mode slices are split into tasks of at most this many entries and
+ * combined deterministically.  Must be set before a mode layout is built. */
+int cpfit_pattern_set_task_size(cpfit_pattern *p, int64_t entries);
+
+/* Stable grouping by mode index (built once, cached in the pattern):
+ * perm int32[nnz] lists entry positions grouped by mode index, stable within
+ * groups; offsets int64[dims[mode]+1].  Bit-exact with
+ * counting_sort_by_mode (core.py:234-249) / SparseTensor.mode_group
+ * (core.py:147-157).  Device radix sort; no host round trip of entries. */
+int cpfit_pattern_mode_group(cpfit_pattern *p, int mode, void *stream,
+                             const int32_t **perm, const int64_t **offsets);
+
+/* Work-table statistics of the mode layout (built on demand): number of
+ * tasks, of split slices (needing the fix-up pass) and of partial slots. */
+int cpfit_pattern_mode_stats(cpfit_pattern *p, int mode, void *stream,
+                             int64_t *ntasks, int64_t *nsplit, int64_t *nslots);
+
+/* out[k] = vals[perm[k]] (values into the mode-sorted order of `mode`).
+ * Replaces: sorted_vals = t.values[perm] (kernels.py:60). */
+int cpfit_permute_values(cpfit_pattern *p, int mode, int dtype,
+                         const void *vals, void *out, void *stream);
+
+/* ---- kernels ---------------------------------------------------------- */
+
+/* TTTP: out[e] = vals[e] * sum_r prod_{n: factors[n] != NULL}
+ *                  factors[n][coords_n[e], r].
+ * Replaces: kernels.tttp (kernels.py:105-149), _jit.tttp3 (_jit.py:49-59). */
+int cpfit_tttp(cpfit_pattern *p, int dtype, int rank, const void *vals,
+               const void *const *factors, void *out, void *stream);
+
+/* MTTKRP: out[i, r] = sum_{e: i_mode(e) = i} vals[e] * prod_{k != mode}
+ *                       factors[k][i_k(e), r];  rows without entries are 0.
+ * `vals_sorted` != 0 means `vals` is already in the mode-sorted order
+ * (cpfit_permute_values), otherwise it is in canonical order.
+ * Replaces: kernels.mttkrp (kernels.py:46-91), _jit.mttkrp3 (_jit.py:35-47). */
+int cpfit_mttkrp(cpfit_pattern *p, int mode, int dtype, int rank,
+                 const void *vals, int vals_sorted,
+                 const void *const *factors, void *out, void *stream);
+
+/* Per-row Gram blocks G_i = sum_{e in row i} w_e h_e h_e^T with
+ * h_e = prod_{k != mode} factors[k][i_k(e), :]  (weights NULL = unit mask).
+ * Writes gram_out[dims[mode] * rank * rank].  Negative weights ->
+ * CPFIT_ENEGWEIGHT.  Replaces: kernels.gram_blocks (kernels.py:159-212). */
+int cpfit_gram(cpfit_pattern *p, int mode, int dtype, int rank,
+               const void *weights, int weights_sorted,
+               const void *const *factors, void *gram_out, void *stream);
+
+/* Per-row regularised normal equations (G_i + reg I) x_i = rhs_i with the
+ * reference's empty-row and singular-row semantics; *bad_row receives the
+ * offending row on CPFIT_EEMPTYROW / CPFIT_ESINGULAR.  gram_out (nullable)
+ * receives G.  Replaces: kernels.solve_factor (kernels.py:215-267). */
+int cpfit_solve_factor(cpfit_pattern *p, int mode, int dtype, int rank,
+                       const void *weights, int weights_sorted,
+                       const void *const *factors, const void *rhs,
+                       double reg, void *x_out, void *gram_out,
+                       int64_t *bad_row, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CPFIT_B200_H */

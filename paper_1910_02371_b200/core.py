@@ -1,0 +1,538 @@
+"""Sparse tensors with a device-resident sparsity pattern.
+
+Same public surface as the reference's core.py (``SparseTensor``,
+``RngState``, ``linearize[_many]``, ``delinearize[_many]``, ``from_coords``,
+``build_tensor``, ``counting_sort_by_mode``, ``model_values``,
+``gen_low_rank``), re-designed around the B200: the first kernel call on a
+tensor uploads its sorted uint64 keys once and builds a *device pattern*
+(``libcpfit_b200``: int32 coordinates per mode, delinearized on the GPU),
+and every mode grouping (stable radix sort, segment offsets, work tasks) is
+built on the device on first use and cached in that pattern.  Tensors made
+with ``with_values`` share the pattern exactly like the reference shares its
+``_coords`` / ``_groups`` caches (core.py:159-167), so ALS/CCD/SGD sweeps
+never re-sort.  Values live on the device per dtype; host ``keys`` /
+``values`` are materialised lazily for device-born tensors (samples, kernel
+outputs).
+
+Host-side helpers (linearize on a tuple, ingest sorting/duplicate merging in
+``from_coords``, synthetic generators) stay numpy, as in the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .exceptions import DataError
+from .validation import check_mode, check_shape
+
+DEFAULT_CELL_CAP = 1 << 26
+
+
+# ---------------------------------------------------------------------------
+# device plumbing (torch = device memory + streams)
+
+def _torch():
+    import torch
+    return torch
+
+
+def cuda_device():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("cpfit-b200 kernels need a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def current_stream() -> int:
+    return _torch().cuda.current_stream().cuda_stream
+
+
+class _CudaArray:
+    """Zero-copy __cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {
+            "shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+            "version": 3, "strides": None, "stream": None,
+        }
+
+
+def device_view(ptr: int, n: int, typestr: str, owner=None):
+    """torch view of library-owned memory (keep ``owner`` alive while used)."""
+    torch = _torch()
+    t = torch.as_tensor(_CudaArray(ptr, n, typestr), device=cuda_device())
+    return t
+
+
+class DevicePattern:
+    """Owner of one ``cpfit_pattern`` handle (device coords + cached layouts)."""
+
+    def __init__(self, shape, nnz: int, handle: int, task_size: int | None = None):
+        self.shape = tuple(shape)
+        self.nnz = int(nnz)
+        self.handle = ctypes.c_void_p(handle)
+        if task_size is not None:
+            _lib.check(_lib.load().cpfit_pattern_set_task_size(self.handle, int(task_size)))
+
+    @classmethod
+    def from_keys(cls, shape, keys):
+        """Upload sorted uint64 keys (numpy or CUDA tensor) and delinearize."""
+        torch = _torch()
+        dev = cuda_device()
+        if isinstance(keys, np.ndarray):
+            k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.uint64).view(np.int64))
+            k = k.to(dev, non_blocking=False)
+        else:
+            k = keys.to(dev).view(torch.int64).contiguous()
+        dims = (ctypes.c_int64 * len(shape))(*shape)
+        out = ctypes.c_void_p()
+        _lib.check(_lib.load().cpfit_pattern_create(
+            len(shape), dims, int(k.numel()), ctypes.c_void_p(k.data_ptr()),
+            ctypes.c_void_p(current_stream()), ctypes.byref(out)), "pattern_create")
+        # keys are consumed by the delinearize kernel on the current stream;
+        # keep them alive until it has run
+        _torch().cuda.current_stream().synchronize()
+        return cls(shape, int(k.numel()), out.value)
+
+    @classmethod
+    def from_device_coords(cls, shape, coords):
+        """Pattern from per-mode int32 CUDA coordinate tensors (canonical order)."""
+        n = int(coords[0].numel()) if coords else 0
+        dims = (ctypes.c_int64 * len(shape))(*shape)
+        arr = _lib.ptr_array([c.data_ptr() for c in coords])
+        out = ctypes.c_void_p()
+        _lib.check(_lib.load().cpfit_pattern_create_coords(
+            len(shape), dims, n, arr, ctypes.c_void_p(current_stream()),
+            ctypes.byref(out)), "pattern_create_coords")
+        _torch().cuda.current_stream().synchronize()
+        return cls(shape, n, out.value)
+
+    def coords(self, mode: int):
+        p = ctypes.c_void_p()
+        _lib.check(_lib.load().cpfit_pattern_coords(self.handle, int(mode), ctypes.byref(p)))
+        return device_view(p.value, self.nnz, "<i4", self)
+
+    def mode_group(self, mode: int):
+        perm = ctypes.c_void_p()
+        offs = ctypes.c_void_p()
+        _lib.check(_lib.load().cpfit_pattern_mode_group(
+            self.handle, int(mode), ctypes.c_void_p(current_stream()), ctypes.byref(perm),
+            ctypes.byref(offs)), "mode_group")
+        return (device_view(perm.value, self.nnz, "<i4", self),
+                device_view(offs.value, self.shape[mode] + 1, "<i8", self))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and _lib._lib is not None:
+            try:
+                _lib.load().cpfit_pattern_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.handle = None
+
+
+@dataclass
+class _Shared:
+    """Pattern-level caches shared through ``with_values`` (core.py:159-167)."""
+
+    coords: tuple | None = None          # host int64 coords (on request)
+    groups: dict = field(default_factory=dict)  # host (perm, offsets) per mode
+    pattern: DevicePattern | None = None
+    task_size: int | None = None
+
+
+def _dtype_code(dtype) -> int:
+    torch = _torch()
+    if dtype == torch.float64:
+        return _lib.F64
+    if dtype == torch.float32:
+        return _lib.F32
+    raise ValueError(f"unsupported dtype {dtype}")
+
+
+# ---------------------------------------------------------------------------
+# RNG (core.py:25-46)
+
+@dataclass(frozen=True)
+class RngState:
+    """Splittable counter-based stream: numpy Philox4x64-10 keyed by
+    SeedSequence(seed, spawn_key=path), identical to the reference."""
+
+    seed: int
+    path: tuple[int, ...] = field(default=())
+    algorithm: str = "philox"
+
+    def generator(self) -> np.random.Generator:
+        ss = np.random.SeedSequence(entropy=self.seed, spawn_key=self.path)
+        return np.random.Generator(np.random.Philox(ss))
+
+    def child(self, key: int) -> "RngState":
+        return RngState(self.seed, self.path + (int(key),), self.algorithm)
+
+    def split(self, n: int) -> list["RngState"]:
+        return [self.child(i) for i in range(n)]
+
+    def philox_key(self) -> tuple[int, int]:
+        """The 2x64-bit Philox key (what the device sampler consumes)."""
+        ss = np.random.SeedSequence(entropy=self.seed, spawn_key=self.path)
+        key = np.random.Philox(ss).state["state"]["key"]
+        return int(key[0]), int(key[1])
+
+
+# ---------------------------------------------------------------------------
+# index arithmetic (core.py:49-102; host utilities)
+
+def linearize(coords, dims) -> int:
+    dims = check_shape(dims)
+    if len(coords) != len(dims):
+        raise ValueError(f"expected {len(dims)} coordinates, got {len(coords)}")
+    key = 0
+    for n, (c, d) in enumerate(zip(coords, dims)):
+        c = int(c)
+        if not 0 <= c < d:
+            raise ValueError(f"coordinate {c} out of range [0, {d}) in mode {n}")
+        key = key * d + c
+    return key
+
+
+def delinearize(key: int, dims) -> tuple[int, ...]:
+    dims = check_shape(dims)
+    key = int(key)
+    if not 0 <= key < math.prod(dims):
+        raise ValueError(f"key {key} out of range for shape {dims}")
+    coords = [0] * len(dims)
+    for n in range(len(dims) - 1, -1, -1):
+        key, coords[n] = divmod(key, dims[n])
+    return tuple(coords)
+
+
+def linearize_many(coord_arrays, dims) -> np.ndarray:
+    dims = check_shape(dims)
+    if len(coord_arrays) != len(dims):
+        raise ValueError("one coordinate array per mode required")
+    n_entries = len(coord_arrays[0]) if len(coord_arrays) else 0
+    keys = np.zeros(n_entries, dtype=np.uint64)
+    for n, (c, d) in enumerate(zip(coord_arrays, dims)):
+        c = np.asarray(c)
+        if c.size and (c.min() < 0 or c.max() >= d):
+            raise ValueError(f"coordinate out of range [0, {d}) in mode {n}")
+        keys = keys * np.uint64(d) + c.astype(np.uint64)
+    return keys
+
+
+def delinearize_many(keys, dims) -> tuple[np.ndarray, ...]:
+    dims = check_shape(dims)
+    rem = np.asarray(keys, dtype=np.uint64).copy()
+    coords = [None] * len(dims)
+    for n in range(len(dims) - 1, -1, -1):
+        d = np.uint64(dims[n])
+        coords[n] = (rem % d).astype(np.int64)
+        rem //= d
+    return tuple(coords)
+
+
+# ---------------------------------------------------------------------------
+# SparseTensor
+
+class SparseTensor:
+    """Order-N sparse tensor in sorted linearized-key coordinate format.
+
+    Invariants (core.py:105-131): keys strictly increasing uint64, every key
+    < prod(dims), len(keys) == len(values); explicit zeros are retained.
+    """
+
+    __slots__ = ("shape", "_keys", "_values", "_shared", "_dvals", "_sorted",
+                 "_keys_fn", "_nnz", "__weakref__")
+
+    def __init__(self, shape, keys, values, validate: bool = True):
+        shape = check_shape(shape)
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        if validate:
+            if keys.ndim != 1 or values.ndim != 1 or keys.shape != values.shape:
+                raise ValueError("keys and values must be 1-D of equal length")
+            if keys.size:
+                if np.any(keys[1:] <= keys[:-1]):
+                    raise ValueError("keys must be strictly increasing")
+                if int(keys[-1]) >= math.prod(shape):
+                    raise ValueError("key out of range for shape")
+        self.shape = shape
+        self._keys = keys
+        self._values = values
+        self._nnz = int(keys.size)
+        self._shared = _Shared()
+        self._dvals = {}
+        self._sorted = {}
+        self._keys_fn = None
+
+    # -- construction of device-born tensors --------------------------------
+    @classmethod
+    def _device_born(cls, shape, nnz, shared, dvalues, keys_fn=None, host_values=None):
+        t = cls.__new__(cls)
+        t.shape = tuple(shape)
+        t._keys = None
+        t._values = host_values
+        t._nnz = int(nnz)
+        t._shared = shared
+        t._dvals = {} if dvalues is None else {dvalues.dtype: dvalues}
+        t._sorted = {}
+        t._keys_fn = keys_fn
+        return t
+
+    @property
+    def keys(self) -> np.ndarray:
+        if self._keys is None:
+            self._keys = np.ascontiguousarray(self._keys_fn(), dtype=np.uint64)
+        return self._keys
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._values is None:
+            torch = _torch()
+            dv = self._dvals.get(torch.float64)
+            if dv is None:
+                dv = next(iter(self._dvals.values()))
+            self._values = dv.to(torch.float64).cpu().numpy()
+        return self._values
+
+    @property
+    def order(self) -> int:
+        return len(self.shape)
+
+    @property
+    def nnz(self) -> int:
+        return self._nnz
+
+    # -- device side ----------------------------------------------------------
+    def device_pattern(self) -> DevicePattern:
+        sh = self._shared
+        if sh.pattern is None:
+            sh.pattern = DevicePattern.from_keys(self.shape, self.keys)
+            if sh.task_size is not None:
+                _lib.check(_lib.load().cpfit_pattern_set_task_size(sh.pattern.handle,
+                                                                  int(sh.task_size)))
+        return sh.pattern
+
+    def set_task_size(self, entries: int) -> None:
+        """Entries per segmented-work task (before the first mode grouping)."""
+        self._shared.task_size = int(entries)
+        if self._shared.pattern is not None:
+            _lib.check(_lib.load().cpfit_pattern_set_task_size(
+                self._shared.pattern.handle, int(entries)))
+
+    def device_values(self, dtype=None):
+        """Values on the device in canonical (key) order, cached per dtype."""
+        torch = _torch()
+        dtype = dtype or torch.float64
+        dv = self._dvals.get(dtype)
+        if dv is None:
+            src = next(iter(self._dvals.values()), None)
+            if src is not None:
+                dv = src.to(dtype)
+            else:
+                dv = torch.from_numpy(self.values).to(cuda_device()).to(dtype)
+            self._dvals[dtype] = dv
+        return dv
+
+    def sorted_values(self, mode: int, dtype=None):
+        """Values permuted into the mode-sorted order of ``mode`` (cached)."""
+        torch = _torch()
+        dtype = dtype or torch.float64
+        key = (int(mode), dtype)
+        sv = self._sorted.get(key)
+        if sv is None:
+            src = self.device_values(dtype)
+            sv = torch.empty_like(src)
+            _lib.check(_lib.load().cpfit_permute_values(
+                self.device_pattern().handle, int(mode), _dtype_code(dtype),
+                ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(sv.data_ptr()),
+                ctypes.c_void_p(current_stream())), "permute_values")
+            self._sorted[key] = sv
+        return sv
+
+    # -- reference API --------------------------------------------------------
+    def coords(self) -> tuple[np.ndarray, ...]:
+        """Per-mode int64 coordinates (device delinearize, cached)."""
+        sh = self._shared
+        if sh.coords is None:
+            if self.nnz == 0:
+                sh.coords = tuple(np.zeros(0, dtype=np.int64) for _ in self.shape)
+            else:
+                pat = self.device_pattern()
+                sh.coords = tuple(pat.coords(n).cpu().numpy().astype(np.int64)
+                                  for n in range(self.order))
+        return sh.coords
+
+    def mode_group(self, mode: int):
+        """Cached (perm, offsets) grouping by mode index (device radix sort;
+        bit-exact with counting_sort_by_mode, core.py:234-249)."""
+        mode = check_mode(mode, self.order)
+        hit = self._shared.groups.get(mode)
+        if hit is None:
+            if self.nnz == 0:
+                hit = (np.zeros(0, dtype=np.int64),
+                       np.zeros(self.shape[mode] + 1, dtype=np.int64))
+            else:
+                perm, offs = self.device_pattern().mode_group(mode)
+                hit = (perm.cpu().numpy().astype(np.int64), offs.cpu().numpy().copy())
+            self._shared.groups[mode] = hit
+        return hit
+
+    def with_values(self, values) -> "SparseTensor":
+        """New tensor sharing this pattern (and its device layouts)."""
+        if type(values).__module__.startswith("torch"):
+            if tuple(values.shape) != (self.nnz,):
+                raise ValueError("values length must match nnz")
+            return SparseTensor._device_born(
+                self.shape, self.nnz, self._shared, values.contiguous(),
+                keys_fn=lambda: self.keys)
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        if values.shape != (self.nnz,):
+            raise ValueError("values length must match nnz")
+        out = SparseTensor._device_born(self.shape, self.nnz, self._shared, None,
+                                        keys_fn=lambda: self.keys, host_values=values)
+        if self._keys is not None:
+            out._keys = self._keys
+        return out
+
+    def observation_mask(self) -> "SparseTensor":
+        """Unit-valued tensor on the same pattern (core.py:169-171)."""
+        if self._values is None and self._dvals:
+            torch = _torch()
+            return self.with_values(torch.ones(self.nnz, dtype=torch.float64,
+                                               device=cuda_device()))
+        return self.with_values(np.ones(self.nnz))
+
+    def sample(self, rate: float, rng: RngState) -> "SparseTensor":
+        """Keep each entry independently with probability ``rate`` (device
+        Philox4x64-10, bit-exact with the reference's core.py:173-183)."""
+        from .sampling import sample_tensor
+        return sample_tensor(self, rate, rng)
+
+    def norm_sq(self) -> float:
+        return float(np.dot(self.values, self.values))
+
+    def __repr__(self) -> str:
+        return f"SparseTensor(shape={self.shape}, nnz={self.nnz})"
+
+
+def build_tensor(entries, shape) -> SparseTensor:
+    """core.py:192-205: unsorted ((coords...), value) pairs, duplicates summed."""
+    shape = check_shape(shape)
+    if not entries:
+        return SparseTensor(shape, np.empty(0, np.uint64), np.empty(0))
+    keys = np.fromiter((linearize(c, shape) for c, _ in entries), dtype=np.uint64,
+                       count=len(entries))
+    values = np.fromiter((v for _, v in entries), dtype=np.float64, count=len(entries))
+    return _merge_sorted(shape, keys, values)
+
+
+def from_coords(coord_arrays, values, shape) -> SparseTensor:
+    """core.py:208-218: per-mode coordinate arrays, duplicates summed."""
+    shape = check_shape(shape)
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    keys = linearize_many(coord_arrays, shape)
+    if keys.shape != values.shape:
+        raise ValueError("coordinate arrays and values must have equal length")
+    return _merge_sorted(shape, keys, values)
+
+
+def _merge_sorted(shape, keys, values) -> SparseTensor:
+    """core.py:221-231: stable key sort, duplicates summed in stable order."""
+    if keys.size == 0:
+        return SparseTensor(shape, keys, values, validate=False)
+    order = np.argsort(keys, kind="stable")
+    keys = keys[order]
+    values = values[order]
+    starts = np.flatnonzero(np.concatenate(([True], keys[1:] != keys[:-1])))
+    if starts.size != keys.size:
+        values = np.add.reduceat(values, starts)
+        keys = keys[starts]
+    return SparseTensor(shape, keys, values, validate=False)
+
+
+def counting_sort_by_mode(t: SparseTensor, mode: int):
+    """Stable grouping of entry positions by mode index -> (perm, offsets).
+
+    Computed on the device (LSD radix sort, core.py:234-249 semantics)."""
+    mode = check_mode(mode, t.order)
+    return t.mode_group(mode)
+
+
+def model_values(factors, coord_arrays, col_block: int = 32) -> np.ndarray:
+    """core.py:252-266: multilinear inner products at given coordinates."""
+    n_entries = len(coord_arrays[0]) if len(coord_arrays) else 0
+    factors = [np.asarray(f.cpu().numpy() if hasattr(f, "cpu") else f, dtype=np.float64)
+               for f in factors]
+    rank = factors[0].shape[1]
+    out = np.zeros(n_entries)
+    for lo in range(0, rank, col_block):
+        hi = min(lo + col_block, rank)
+        prod = factors[0][coord_arrays[0], lo:hi].copy()
+        for n in range(1, len(factors)):
+            prod *= factors[n][coord_arrays[n], lo:hi]
+        out += prod.sum(axis=1)
+    return out
+
+
+def gen_low_rank(shape, rank: int, observed_fraction: float,
+                 value_law: str = "uniform01", rng: RngState | None = None,
+                 cell_cap: int = DEFAULT_CELL_CAP):
+    """core.py:269-314 (host synthesis; identical draws to the reference)."""
+    shape = check_shape(shape)
+    if not 0.0 < observed_fraction <= 1.0:
+        raise ValueError("observed_fraction must be in (0, 1]")
+    total = math.prod(shape)
+    if total > cell_cap:
+        raise DataError(f"cell space {total} exceeds enumeration cap {cell_cap}; "
+                        "raise cell_cap explicitly for larger masks")
+    if rng is None:
+        rng = RngState(0)
+    g = rng.generator()
+    factors = []
+    for d in shape:
+        if value_law == "uniform01":
+            factors.append(g.random((d, rank)))
+        elif value_law == "gaussian":
+            factors.append(g.standard_normal((d, rank)))
+        else:
+            raise ValueError(f"unknown value_law {value_law!r}")
+    if observed_fraction >= 1.0:
+        keys = np.arange(total, dtype=np.uint64)
+    else:
+        keys = np.flatnonzero(g.random(total) < observed_fraction).astype(np.uint64)
+    coords = delinearize_many(keys, shape)
+    values = model_values(factors, coords)
+    t = SparseTensor(shape, keys, values, validate=False)
+    return t, factors
+
+
+def gen_function_tensor(shape, observed_fraction: float, rng: RngState | None = None,
+                        func=None, cell_cap: int = DEFAULT_CELL_CAP) -> SparseTensor:
+    """core.py:317-348 placeholder generator (host)."""
+    shape = check_shape(shape)
+    if not 0.0 < observed_fraction <= 1.0:
+        raise ValueError("observed_fraction must be in (0, 1]")
+    total = math.prod(shape)
+    if total > cell_cap:
+        raise DataError(f"cell space {total} exceeds enumeration cap {cell_cap}")
+    if rng is None:
+        rng = RngState(0)
+    if func is None:
+        def func(coords):
+            s = np.zeros(len(coords[0]))
+            for c in coords:
+                s += c
+            return 1.0 / (1.0 + s)
+    g = rng.generator()
+    if observed_fraction >= 1.0:
+        keys = np.arange(total, dtype=np.uint64)
+    else:
+        keys = np.flatnonzero(g.random(total) < observed_fraction).astype(np.uint64)
+    return SparseTensor(shape, keys, func(delinearize_many(keys, shape)), validate=False)

@@ -1,0 +1,202 @@
+// common.cuh -- shared helpers for the sm_100a kernels of cpfit-b200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/cpfit_b200.h"
+
+#define CPFIT_MAXN 8  // maximum tensor order handled on the device
+
+namespace cpfit {
+
+void set_error(const char *fmt, ...);
+int cuda_status(cudaError_t e, const char *what);
+
+#define CPFIT_CUDA(call)                                       \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return ::cpfit::cuda_status(_e, #call); \
+  } while (0)
+
+#define CPFIT_LAUNCH_CHECK(what)                               \
+  do {                                                         \
+    cudaError_t _e = cudaGetLastError();                       \
+    if (_e != cudaSuccess) return ::cpfit::cuda_status(_e, what); \
+  } while (0)
+
+#define CPFIT_TRY(call)          \
+  do {                           \
+    int _s = (call);             \
+    if (_s != CPFIT_OK) return _s; \
+  } while (0)
+
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// Stream-ordered scratch allocation (the device's default memory pool).
+template <typename T>
+inline int dalloc(T **p, size_t count, cudaStream_t s) {
+  *p = nullptr;
+  if (count == 0) return CPFIT_OK;
+  cudaError_t e = cudaMallocAsync((void **)p, count * sizeof(T), s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation of %zu bytes failed: %s", count * sizeof(T),
+              cudaGetErrorString(e));
+    return CPFIT_ENOMEM;
+  }
+  return CPFIT_OK;
+}
+
+template <typename T>
+inline void dfree(T *p, cudaStream_t s) {
+  if (p) cudaFreeAsync((void *)p, s);
+}
+
+// RAII holder for stream-ordered scratch.
+template <typename T>
+struct Scratch {
+  T *ptr = nullptr;
+  cudaStream_t s = nullptr;
+  Scratch() = default;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  int alloc(size_t n) { return dalloc(&ptr, n, s); }
+  ~Scratch() { dfree(ptr, s); }
+  Scratch(const Scratch &) = delete;
+  Scratch &operator=(const Scratch &) = delete;
+};
+
+// ---- vector loads ---------------------------------------------------------
+template <typename T, int VEC>
+struct VecT;
+template <> struct VecT<double, 1> { typedef double type; };
+template <> struct VecT<double, 2> { typedef double2 type; };
+template <> struct VecT<float, 1> { typedef float type; };
+template <> struct VecT<float, 2> { typedef float2 type; };
+template <> struct VecT<float, 4> { typedef float4 type; };
+
+template <typename T, int VEC>
+__device__ __forceinline__ void load_vec(const T *__restrict__ p, T (&v)[VEC]) {
+  typedef typename VecT<T, VEC>::type V;
+  V x = __ldg(reinterpret_cast<const V *>(p));
+  if constexpr (VEC == 1) {
+    v[0] = x;
+  } else if constexpr (VEC == 2) {
+    v[0] = x.x; v[1] = x.y;
+  } else {
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void store_vec(T *__restrict__ p, const T (&v)[VEC]) {
+  typedef typename VecT<T, VEC>::type V;
+  V x;
+  if constexpr (VEC == 1) {
+    x = v[0];
+  } else if constexpr (VEC == 2) {
+    x.x = v[0]; x.y = v[1];
+  } else {
+    x.x = v[0]; x.y = v[1]; x.z = v[2]; x.w = v[3];
+  }
+  *reinterpret_cast<V *>(p) = x;
+}
+
+__device__ __forceinline__ double shfl_xor(double v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+__device__ __forceinline__ float shfl_xor(float v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+
+// Column-tiling of a rank-R row across a lane group: each of LPE lanes
+// handles KV vectors of VEC contiguous columns, columns (k*LPE + q)*VEC.
+struct RowTiling {
+  int vec, lpe, kv;
+};
+
+template <typename T>
+inline int pick_vec(int rank, const void *const *ptrs, int n) {
+  size_t row_bytes = (size_t)rank * sizeof(T);
+  int vec = 1;
+  if (row_bytes % 16 == 0)
+    vec = 16 / (int)sizeof(T);
+  else if (row_bytes % 8 == 0 && sizeof(T) == 4)
+    vec = 2;
+  for (int i = 0; i < n; ++i)
+    if (ptrs[i] && ((uintptr_t)ptrs[i] % (vec * sizeof(T)) != 0)) vec = 1;
+  return vec;
+}
+
+inline RowTiling pick_tiling(int rank, int vec, int kvmax) {
+  RowTiling t;
+  t.vec = vec;
+  int nv = (rank + vec - 1) / vec;  // vectors per row
+  int lpe = 4;
+  while (lpe < nv && lpe < 32) lpe *= 2;
+  t.lpe = lpe;
+  t.kv = (nv + lpe - 1) / lpe;
+  if (t.kv > kvmax) t.kv = -1;
+  return t;
+}
+
+// ---- device scan (exclusive, int64 out) -----------------------------------
+// out[i] = sum_{j<i} in[j] for i in [0, n]; out has n+1 entries (out[n] = total).
+template <typename Tin>
+int exclusive_scan(const Tin *in, int64_t *out, int64_t n, cudaStream_t s);
+
+// gather: out[k] = in[idx[k]]
+int gather_i32(const int32_t *in, const int32_t *idx, int32_t *out, int64_t n,
+               cudaStream_t s);
+
+inline unsigned grid_for(int64_t work, int threads, int per_thread = 1) {
+  int64_t b = (work + (int64_t)threads * per_thread - 1) / ((int64_t)threads * per_thread);
+  int64_t cap = (int64_t)num_sms() * 32;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+}  // namespace cpfit
+
+// Opaque pattern handle (C-ABI) -- defined here for the kernel files.
+struct CpfitModeLayout {
+  bool built = false;
+  int32_t *perm = nullptr;        // nnz (mode-sorted position -> entry); null = identity
+  int64_t *offsets = nullptr;     // dim + 1
+  int32_t *sorted_idx[CPFIT_MAXN] = {nullptr};  // coords of each mode, mode-sorted order
+  bool owns_sorted[CPFIT_MAXN] = {false};
+  // segmented-work tasks
+  int64_t ntasks = 0, nslots = 0, nsplit = 0, task_size = 0;
+  int64_t *task_begin = nullptr;  // ntasks + 1
+  int32_t *task_row = nullptr;    // ntasks
+  int32_t *task_slot = nullptr;   // ntasks (-1 = row owned by one task)
+  int32_t *split_row = nullptr;   // nsplit
+  int32_t *split_slot = nullptr;  // nsplit + 1
+  int32_t *identity_perm = nullptr;  // materialised on request for mode 0
+};
+
+struct cpfit_pattern {
+  int order = 0;
+  int64_t dims[CPFIT_MAXN] = {0};
+  int64_t nnz = 0;
+  int32_t *coords[CPFIT_MAXN] = {nullptr};
+  int64_t task_size = 1024;
+  CpfitModeLayout modes[CPFIT_MAXN];
+};
+
+namespace cpfit {
+int ensure_layout(cpfit_pattern *p, int mode, cudaStream_t s);
+}

@@ -1,0 +1,620 @@
+// gram_solve.cu -- per-row normal-equation blocks (Gram) and the batched
+// small-SPD solve of ALS completion, for sm_100a.
+//
+// Gram: G_i = sum_{e in row i} (sqrt(w_e) h_e)(sqrt(w_e) h_e)^T with
+// h_e = prod_{k != mode} A_k[i_k(e), :] -- exactly the reference's staged
+// rank-k update (kernels.py:195-205).  One warp per mode-sorted task stages
+// 32 Hadamard rows at a time in shared memory and accumulates G with FP64
+// tensor-core MMAs (mma.sync m8n8k4 f64 -> DMMA; tcgen05 has no f64 kind),
+// computing only the upper-triangular 8x8 tiles (G is symmetric) and
+// mirroring on store.  Long rows are split into tasks whose partial Grams
+// are summed in task order (deterministic; no floating-point atomics).
+//
+// Solve: one warp per row factors (G_i + reg I) with a shared-memory
+// Cholesky; a row whose Cholesky hits a non-positive pivot is re-solved with
+// partial-pivoting LU, which reports "singular" exactly when LAPACK gesv
+// (np.linalg.solve, kernels.py:259) would: on an exact zero pivot.  Empty
+// rows follow kernels.py:245-257 (x = rhs/reg, or identity when reg == 0 with
+// an error for a nonzero rhs).  The first offending row is found with an
+// integer atomicMin (order independent).
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace cpfit {
+
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+template <typename T>
+struct GramParams {
+  int np;
+  int rank;
+  const int32_t *idx[CPFIT_MAXN];  // mode-sorted coordinates of the other modes
+  const T *fac[CPFIT_MAXN];
+  const T *weights;       // nullable (unit weights)
+  const int32_t *wperm;   // non-null: weights in canonical order, gather by perm
+  const int64_t *task_begin;
+  const int32_t *task_row;
+  const int32_t *task_slot;
+  int64_t ntasks;
+  T *gram;      // dims[mode] x R x R
+  T *partial;   // nslots x R x R
+};
+
+constexpr int GRAM_WARPS = 4;
+constexpr int GRAM_CHUNK = 32;  // Hadamard rows staged per MMA sweep
+
+template <int RT>
+constexpr int gram_ld() {
+  return RT * 8 + 8;  // +8 doubles: rows 64 B apart in bank space
+}
+
+template <typename T, int RT>
+__global__ void __launch_bounds__(GRAM_WARPS * 32)
+gram_kernel(const GramParams<T> p) {
+  constexpr int RP = RT * 8;
+  constexpr int LD = gram_ld<RT>();
+  constexpr int NT = RT * (RT + 1) / 2;  // upper-triangular tiles
+  extern __shared__ double gsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double *H = gsm + (size_t)wib * GRAM_CHUNK * LD;
+  const int rank = p.rank;
+  const int64_t warp = (int64_t)blockIdx.x * GRAM_WARPS + wib;
+  const int64_t nwarps = (int64_t)gridDim.x * GRAM_WARPS;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  for (int64_t t = warp; t < p.ntasks; t += nwarps) {
+    const int64_t b0 = p.task_begin[t], b1 = p.task_begin[t + 1];
+    double acc[NT][2];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = 0.0;
+
+    for (int64_t base = b0; base < b1; base += GRAM_CHUNK) {
+      const int cnt = (int)(b1 - base < GRAM_CHUNK ? b1 - base : GRAM_CHUNK);
+      // coalesced index / weight loads, one entry per lane
+      const int64_t e = base + lane;
+      int32_t my_idx[CPFIT_MAXN];
+#pragma unroll
+      for (int n = 0; n < CPFIT_MAXN; ++n)
+        my_idx[n] = (n < p.np && lane < cnt) ? __ldg(p.idx[n] + e) : 0;
+      double my_sw = 1.0;
+      if (p.weights && lane < cnt) {
+        T w = p.wperm ? __ldg(p.weights + __ldg(p.wperm + e)) : __ldg(p.weights + e);
+        my_sw = sqrt((double)w);
+      }
+      // stage sqrt(w) * h rows: the warp gathers one factor row per step
+#pragma unroll 4
+      for (int j = 0; j < GRAM_CHUNK; ++j) {
+        const double sw = __shfl_sync(0xffffffffu, my_sw, j);
+        int rows[CPFIT_MAXN];
+#pragma unroll
+        for (int n = 0; n < CPFIT_MAXN; ++n)
+          if (n < p.np) rows[n] = __shfl_sync(0xffffffffu, my_idx[n], j);
+#pragma unroll
+        for (int c0 = 0; c0 < RP; c0 += 32) {
+          const int c = c0 + lane;
+          double h = 0.0;
+          if (j < cnt && c < rank) {
+#pragma unroll
+            for (int n = 0; n < CPFIT_MAXN; ++n) {
+              if (n >= p.np) break;
+              const double a = (double)__ldg(p.fac[n] + (int64_t)rows[n] * rank + c);
+              h = (n == 0) ? a : h * a;
+            }
+            h *= sw;
+          }
+          if (c < RP) H[j * LD + c] = h;
+        }
+      }
+      __syncwarp();
+      const int kend = (cnt + 3) & ~3;
+      for (int kk = 0; kk < kend; kk += 4) {
+        double f[RT];
+#pragma unroll
+        for (int i = 0; i < RT; ++i) f[i] = H[(kk + tq) * LD + 8 * i + gq];
+        int tile = 0;
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+#pragma unroll
+          for (int j = i; j < RT; ++j) {
+            dmma_8x8x4(acc[tile][0], acc[tile][1], f[i], f[j]);
+            ++tile;
+          }
+      }
+      __syncwarp();
+    }
+    // store the tiles (and their mirror images) as rows of G
+    const int slot = p.task_slot[t];
+    T *dst = slot < 0 ? p.gram + (int64_t)p.task_row[t] * rank * rank
+                      : p.partial + (int64_t)slot * rank * rank;
+    int tile = 0;
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int j = i; j < RT; ++j) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int r = 8 * i + gq, c = 8 * j + 2 * tq + v;
+          if (r < rank && c < rank) {
+            dst[(int64_t)r * rank + c] = (T)acc[tile][v];
+            if (i != j) dst[(int64_t)c * rank + r] = (T)acc[tile][v];
+          }
+        }
+        ++tile;
+      }
+  }
+}
+
+template <typename T>
+__global__ void combine_gram_partials(const int32_t *__restrict__ split_row,
+                                      const int32_t *__restrict__ split_slot, int64_t nsplit,
+                                      int64_t rr, const T *__restrict__ partial,
+                                      T *__restrict__ gram) {
+  const int64_t blk = blockIdx.x;
+  for (int64_t s = blk; s < nsplit; s += gridDim.x) {
+    const int64_t row = split_row[s];
+    const int64_t a = split_slot[s], b = split_slot[s + 1];
+    for (int64_t c = threadIdx.x; c < rr; c += blockDim.x) {
+      double acc = (double)partial[a * rr + c];
+      for (int64_t k = a + 1; k < b; ++k) acc += (double)partial[k * rr + c];
+      gram[row * rr + c] = (T)acc;
+    }
+  }
+}
+
+template <typename T>
+__global__ void check_weights_kernel(const T *__restrict__ w, int64_t n, int *flag) {
+  int bad = 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    bad |= (w[k] < T(0));
+  bad = __syncthreads_or(bad);
+  if (bad && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+template <typename T, int RT>
+static int launch_gram_rt(const GramParams<T> &p, cudaStream_t s) {
+  constexpr int LD = gram_ld<RT>();
+  const size_t smem = (size_t)GRAM_WARPS * GRAM_CHUNK * LD * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gram_kernel<T, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = true;
+  }
+  int64_t blocks = (p.ntasks + GRAM_WARPS - 1) / GRAM_WARPS;
+  int64_t cap = (int64_t)num_sms() * 8;
+  unsigned grid = (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+  gram_kernel<T, RT><<<grid, GRAM_WARPS * 32, smem, s>>>(p);
+  CPFIT_LAUNCH_CHECK("gram_kernel");
+  return CPFIT_OK;
+}
+
+template <typename T>
+static int launch_gram(const GramParams<T> &p, cudaStream_t s) {
+  switch ((p.rank + 7) / 8) {
+    case 1: return launch_gram_rt<T, 1>(p, s);
+    case 2: return launch_gram_rt<T, 2>(p, s);
+    case 3: return launch_gram_rt<T, 3>(p, s);
+    case 4: return launch_gram_rt<T, 4>(p, s);
+    case 5: return launch_gram_rt<T, 5>(p, s);
+    case 6: return launch_gram_rt<T, 6>(p, s);
+    case 7: return launch_gram_rt<T, 7>(p, s);
+    case 8: return launch_gram_rt<T, 8>(p, s);
+  }
+  set_error("rank %d > 64 is not supported by the Gram kernel", p.rank);
+  return CPFIT_EINVAL;
+}
+
+// Runs the Gram assembly into `gram` (dims[mode] x R x R, zero rows for
+// empty slices).  Weights: nullptr = unit mask.
+template <typename T>
+static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
+                    int weights_sorted, const void *const *factors, T *gram, cudaStream_t s) {
+  const int64_t dim = pt->dims[mode];
+  const int64_t rr = (int64_t)rank * rank;
+  if (weights && pt->nnz > 0) {
+    Scratch<int> flag(s);
+    CPFIT_TRY(flag.alloc(1));
+    CPFIT_CUDA(cudaMemsetAsync(flag.ptr, 0, sizeof(int), s));
+    check_weights_kernel<T><<<grid_for(pt->nnz, 256, 8), 256, 0, s>>>(weights, pt->nnz, flag.ptr);
+    CPFIT_LAUNCH_CHECK("check_weights");
+    int h = 0;
+    CPFIT_CUDA(cudaMemcpyAsync(&h, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CPFIT_CUDA(cudaStreamSynchronize(s));
+    if (h) {
+      set_error("weights must be nonnegative for normal-equation assembly");
+      return CPFIT_ENEGWEIGHT;
+    }
+  }
+  CPFIT_CUDA(cudaMemsetAsync(gram, 0, (size_t)dim * rr * sizeof(T), s));
+  if (pt->nnz == 0) return CPFIT_OK;
+  CPFIT_TRY(ensure_layout(pt, mode, s));
+  CpfitModeLayout &L = pt->modes[mode];
+  GramParams<T> p{};
+  p.rank = rank;
+  int np = 0;
+  for (int n = 0; n < pt->order; ++n) {
+    if (n == mode) continue;
+    if (!factors[n]) {
+      set_error("factor[%d] is required but missing", n);
+      return CPFIT_EINVAL;
+    }
+    p.idx[np] = L.sorted_idx[n];
+    p.fac[np] = (const T *)factors[n];
+    ++np;
+  }
+  if (np == 0) {
+    set_error("at least one factor matrix must be provided");
+    return CPFIT_EINVAL;
+  }
+  p.np = np;
+  p.weights = weights;
+  p.wperm = (weights && !weights_sorted) ? L.perm : nullptr;
+  p.task_begin = L.task_begin;
+  p.task_row = L.task_row;
+  p.task_slot = L.task_slot;
+  p.ntasks = L.ntasks;
+  p.gram = gram;
+  Scratch<T> partial(s);
+  if (L.nslots > 0) CPFIT_TRY(partial.alloc((size_t)L.nslots * rr));
+  p.partial = partial.ptr;
+  CPFIT_TRY(launch_gram<T>(p, s));
+  if (L.nsplit > 0) {
+    unsigned grid = (unsigned)(L.nsplit < 65535 ? L.nsplit : 65535);
+    combine_gram_partials<T><<<grid, 128, 0, s>>>(L.split_row, L.split_slot, L.nsplit, rr,
+                                                  partial.ptr, gram);
+    CPFIT_LAUNCH_CHECK("combine_gram_partials");
+  }
+  return CPFIT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// batched solve
+
+template <typename T>
+struct SolveParams {
+  int rank;
+  int64_t dim;
+  const T *gram;
+  const T *rhs;
+  const int64_t *offsets;
+  double reg;
+  T *x;
+  unsigned long long *bad;  // [0] first empty row with nonzero rhs, [1] first singular row
+};
+
+// Partial-pivot LU of the R x R system in smem (row-major, leading dim ld),
+// right-hand side b[] distributed (element i held by lane i % 32, slot i / 32).
+// Returns false on an exact zero pivot (LAPACK dgetrf info > 0).
+template <int KB>
+__device__ bool warp_lu_solve(double *A, int ld, int R, double (&b)[KB]) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < R; ++k) {
+    // pivot: max |A[i][k]|, lowest index on ties (idamax)
+    double best = -1.0;
+    int bi = R;
+    for (int i = k + lane; i < R; i += 32) {
+      double v = fabs(A[i * ld + k]);
+      if (v > best) { best = v; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const int piv = bi < R ? bi : k;  // all-NaN column: keep k, as idamax would
+    if (A[piv * ld + k] == 0.0) return false;
+    if (piv != k) {
+      for (int j = lane; j < R; j += 32) {
+        double t = A[k * ld + j];
+        A[k * ld + j] = A[piv * ld + j];
+        A[piv * ld + j] = t;
+      }
+      // swap b[k] and b[piv]
+      double bk = 0.0, bp = 0.0;
+#pragma unroll
+      for (int s = 0; s < KB; ++s) {
+        bk = (k / 32 == s) ? __shfl_sync(0xffffffffu, b[s], k % 32) : bk;
+        bp = (piv / 32 == s) ? __shfl_sync(0xffffffffu, b[s], piv % 32) : bp;
+      }
+#pragma unroll
+      for (int s = 0; s < KB; ++s) {
+        if (s * 32 + lane == k) b[s] = bp;
+        if (s * 32 + lane == piv) b[s] = bk;
+      }
+    }
+    __syncwarp();
+    const double akk = A[k * ld + k];
+    double bk = 0.0;
+#pragma unroll
+    for (int s = 0; s < KB; ++s)
+      bk = (k / 32 == s) ? __shfl_sync(0xffffffffu, b[s], k % 32) : bk;
+    // multipliers and rhs update
+#pragma unroll
+    for (int s = 0; s < KB; ++s) {
+      int i = s * 32 + lane;
+      if (i > k && i < R) {
+        double l = A[i * ld + k] / akk;
+        A[i * ld + k] = l;
+        b[s] -= l * bk;
+      }
+    }
+    __syncwarp();
+    const int n = R - k - 1;
+    for (int q = lane; q < n * n; q += 32) {
+      int i = k + 1 + q / n, j = k + 1 + q % n;
+      A[i * ld + j] -= A[i * ld + k] * A[k * ld + j];
+    }
+    __syncwarp();
+  }
+  // back substitution U x = b
+  for (int k = R - 1; k >= 0; --k) {
+    double bk = 0.0;
+#pragma unroll
+    for (int s = 0; s < KB; ++s)
+      bk = (k / 32 == s) ? __shfl_sync(0xffffffffu, b[s], k % 32) : bk;
+    const double xk = bk / A[k * ld + k];
+#pragma unroll
+    for (int s = 0; s < KB; ++s) {
+      int i = s * 32 + lane;
+      if (i == k) b[s] = xk;
+      else if (i < k) b[s] -= A[i * ld + k] * xk;
+    }
+  }
+  return true;
+}
+
+template <typename T, int KB>
+__global__ void solve_kernel(const SolveParams<T> p, int warps_per_block) {
+  extern __shared__ double ssm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int R = p.rank, ld = R + 1;
+  double *A = ssm + (size_t)wib * R * ld;
+  const int64_t warp = (int64_t)blockIdx.x * warps_per_block + wib;
+  const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
+
+  for (int64_t row = warp; row < p.dim; row += nwarps) {
+    const bool empty = p.offsets[row + 1] == p.offsets[row];
+    const T *rhs = p.rhs + row * R;
+    T *xo = p.x + row * R;
+    double b[KB];
+#pragma unroll
+    for (int s = 0; s < KB; ++s) {
+      int i = s * 32 + lane;
+      b[s] = i < R ? (double)rhs[i] : 0.0;
+    }
+    if (empty) {
+      // kernels.py:245-257: reg*I system (x = rhs/reg) or identity when reg == 0
+      bool nz = false;
+#pragma unroll
+      for (int s = 0; s < KB; ++s) {
+        int i = s * 32 + lane;
+        if (i < R) {
+          if (p.reg == 0.0) {
+            nz |= (b[s] != 0.0);
+            xo[i] = (T)b[s];
+          } else {
+            xo[i] = (T)(b[s] / p.reg);
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, nz) && lane == 0) atomicMin(&p.bad[0], (unsigned long long)row);
+      continue;
+    }
+    const T *G = p.gram + row * R * R;
+    for (int q = lane; q < R * R; q += 32) {
+      int i = q / R, j = q % R;
+      A[i * ld + j] = (double)G[q] + (i == j ? p.reg : 0.0);
+    }
+    __syncwarp();
+    // Cholesky (lower, in place)
+    bool ok = true;
+    for (int k = 0; k < R; ++k) {
+      const double d = A[k * ld + k];
+      if (!(d > 0.0) || !(d < DBL_MAX)) { ok = false; break; }
+      const double l = sqrt(d);
+      __syncwarp();
+      for (int i = k + 1 + lane; i < R; i += 32) A[i * ld + k] /= l;
+      if (lane == 0) A[k * ld + k] = l;
+      __syncwarp();
+      const int n = R - k - 1;
+      for (int q = lane; q < n * n; q += 32) {
+        int i = k + 1 + q / n, j = k + 1 + q % n;
+        if (j <= i) A[i * ld + j] -= A[i * ld + k] * A[j * ld + k];
+      }
+      __syncwarp();
+    }
+    if (ok) {
+      // forward L y = b
+      for (int k = 0; k < R; ++k) {
+        double bk = 0.0;
+#pragma unroll
+        for (int s = 0; s < KB; ++s)
+          bk = (k / 32 == s) ? __shfl_sync(0xffffffffu, b[s], k % 32) : bk;
+        const double yk = bk / A[k * ld + k];
+#pragma unroll
+        for (int s = 0; s < KB; ++s) {
+          int i = s * 32 + lane;
+          if (i == k) b[s] = yk;
+          else if (i > k && i < R) b[s] -= A[i * ld + k] * yk;
+        }
+      }
+      // backward L^T x = y
+      for (int k = R - 1; k >= 0; --k) {
+        double bk = 0.0;
+#pragma unroll
+        for (int s = 0; s < KB; ++s)
+          bk = (k / 32 == s) ? __shfl_sync(0xffffffffu, b[s], k % 32) : bk;
+        const double xk = bk / A[k * ld + k];
+#pragma unroll
+        for (int s = 0; s < KB; ++s) {
+          int i = s * 32 + lane;
+          if (i == k) b[s] = xk;
+          else if (i < k) b[s] -= A[k * ld + i] * xk;
+        }
+      }
+    } else {
+      // not numerically positive definite: LU with partial pivoting decides
+      __syncwarp();
+      for (int q = lane; q < R * R; q += 32) {
+        int i = q / R, j = q % R;
+        A[i * ld + j] = (double)G[q] + (i == j ? p.reg : 0.0);
+      }
+#pragma unroll
+      for (int s = 0; s < KB; ++s) {
+        int i = s * 32 + lane;
+        b[s] = i < R ? (double)rhs[i] : 0.0;
+      }
+      __syncwarp();
+      if (!warp_lu_solve<KB>(A, ld, R, b)) {
+        if (lane == 0) atomicMin(&p.bad[1], (unsigned long long)row);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < KB; ++s) {
+      int i = s * 32 + lane;
+      if (i < R) xo[i] = (T)b[s];
+    }
+    __syncwarp();
+  }
+}
+
+template <typename T>
+static int run_solve(cpfit_pattern *pt, int mode, int rank, const T *gram, const T *rhs,
+                     double reg, T *x, int64_t *bad_row, cudaStream_t s) {
+  CpfitModeLayout &L = pt->modes[mode];
+  const int64_t dim = pt->dims[mode];
+  Scratch<unsigned long long> bad(s);
+  CPFIT_TRY(bad.alloc(2));
+  CPFIT_CUDA(cudaMemsetAsync(bad.ptr, 0xff, 2 * sizeof(unsigned long long), s));
+  SolveParams<T> p{};
+  p.rank = rank;
+  p.dim = dim;
+  p.gram = gram;
+  p.rhs = rhs;
+  p.offsets = L.offsets;
+  p.reg = reg;
+  p.x = x;
+  p.bad = bad.ptr;
+  const size_t per_warp = (size_t)rank * (rank + 1) * sizeof(double);
+  int wpb = (int)(49152 / per_warp);
+  if (wpb > 8) wpb = 8;
+  if (wpb < 1) wpb = 1;
+  const size_t smem = per_warp * wpb;
+  int64_t blocks = (dim + wpb - 1) / wpb;
+  int64_t cap = (int64_t)num_sms() * 16;
+  unsigned grid = (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+  const int kb = (rank + 31) / 32;
+#define CPFIT_SOLVE_CASE(K)                                                              \
+  case K: {                                                                              \
+    cudaFuncSetAttribute(solve_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)smem);                                                     \
+    solve_kernel<T, K><<<grid, wpb * 32, smem, s>>>(p, wpb);                             \
+    break;                                                                               \
+  }
+  switch (kb) {
+    CPFIT_SOLVE_CASE(1)
+    CPFIT_SOLVE_CASE(2)
+    CPFIT_SOLVE_CASE(3)
+    CPFIT_SOLVE_CASE(4)
+    default:
+      set_error("rank %d > 128 is not supported by the solve kernel", rank);
+      return CPFIT_EINVAL;
+  }
+#undef CPFIT_SOLVE_CASE
+  CPFIT_LAUNCH_CHECK("solve_kernel");
+  unsigned long long h[2];
+  CPFIT_CUDA(cudaMemcpyAsync(h, bad.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CPFIT_CUDA(cudaStreamSynchronize(s));
+  if (h[0] != ~0ull) {
+    *bad_row = (int64_t)h[0];
+    set_error("mode %d row %lld: no incident entries and reg=0 but right-hand side is nonzero",
+              mode, (long long)h[0]);
+    return CPFIT_EEMPTYROW;
+  }
+  if (h[1] != ~0ull) {
+    *bad_row = (int64_t)h[1];
+    set_error("mode %d row %lld: singular normal equations (reg=%g)", mode, (long long)h[1],
+              reg);
+    return CPFIT_ESINGULAR;
+  }
+  return CPFIT_OK;
+}
+
+template <typename T>
+static int run_solve_factor(cpfit_pattern *pt, int mode, int rank, const void *weights,
+                            int weights_sorted, const void *const *factors, const void *rhs,
+                            double reg, void *x_out, void *gram_out, int64_t *bad_row,
+                            cudaStream_t s) {
+  const int64_t dim = pt->dims[mode];
+  Scratch<T> gtmp(s);
+  T *gram = (T *)gram_out;
+  if (!gram) {
+    CPFIT_TRY(gtmp.alloc((size_t)dim * rank * rank));
+    gram = gtmp.ptr;
+  }
+  // Gram first, then the regularisation check: the reference's error order
+  // (kernels.py:235-243)
+  CPFIT_TRY(run_gram<T>(pt, mode, rank, (const T *)weights, weights_sorted, factors, gram, s));
+  if (reg < 0.0) {
+    set_error("regularization must be >= 0");
+    return CPFIT_EINVAL;
+  }
+  CPFIT_TRY(ensure_layout(pt, mode, s));
+  int64_t dummy = -1;
+  return run_solve<T>(pt, mode, rank, gram, (const T *)rhs, reg, (T *)x_out,
+                      bad_row ? bad_row : &dummy, s);
+}
+
+}  // namespace cpfit
+
+using namespace cpfit;
+
+extern "C" {
+
+int cpfit_gram(cpfit_pattern *p, int mode, int dtype, int rank, const void *weights,
+               int weights_sorted, const void *const *factors, void *gram_out, void *stream) {
+  if (!p || mode < 0 || mode >= p->order) {
+    set_error("mode %d out of range for order-%d tensor", mode, p ? p->order : 0);
+    return CPFIT_EINVAL;
+  }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64)
+    return run_gram<double>(p, mode, rank, (const double *)weights, weights_sorted, factors,
+                            (double *)gram_out, s);
+  if (dtype == CPFIT_F32)
+    return run_gram<float>(p, mode, rank, (const float *)weights, weights_sorted, factors,
+                           (float *)gram_out, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+int cpfit_solve_factor(cpfit_pattern *p, int mode, int dtype, int rank, const void *weights,
+                       int weights_sorted, const void *const *factors, const void *rhs,
+                       double reg, void *x_out, void *gram_out, int64_t *bad_row,
+                       void *stream) {
+  if (!p || mode < 0 || mode >= p->order) {
+    set_error("mode %d out of range for order-%d tensor", mode, p ? p->order : 0);
+    return CPFIT_EINVAL;
+  }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64)
+    return run_solve_factor<double>(p, mode, rank, weights, weights_sorted, factors, rhs, reg,
+                                    x_out, gram_out, bad_row, s);
+  if (dtype == CPFIT_F32)
+    return run_solve_factor<float>(p, mode, rank, weights, weights_sorted, factors, rhs, reg,
+                                   x_out, gram_out, bad_row, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+}  // extern "C"

@@ -1,0 +1,638 @@
+// pattern.cu -- device-resident sparsity pattern: delinearize, stable mode
+// grouping (LSD radix sort), segment offsets and the work-task tables used by
+// the segmented kernels.
+//
+// Reference: SparseTensor caches (core.py:141-167), delinearize_many
+// (core.py:93-102), counting_sort_by_mode (core.py:234-249).
+#include <cstdarg>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+
+namespace cpfit {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char *what) {
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? CPFIT_ENOMEM : CPFIT_ECUDA;
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan (3-phase: tile sums, recursive scan of sums, apply)
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+__device__ __forceinline__ int64_t warp_incl_scan(int64_t v) {
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns exclusive prefix
+// and writes the block total to *total.
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t *total) {
+  __shared__ int64_t warp_sums[SCAN_THREADS / 32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t incl = warp_incl_scan(v);
+  if (lane == 31) warp_sums[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int64_t x = lane < SCAN_THREADS / 32 ? warp_sums[lane] : 0;
+    int64_t xi = warp_incl_scan(x);
+    if (lane < SCAN_THREADS / 32) warp_sums[lane] = xi - x;
+    if (lane == 31) *total = xi;  // lanes >= nwarps add zeros: lane 31 holds the total
+  }
+  __syncthreads();
+  int64_t r = incl - v + warp_sums[w];
+  __syncthreads();
+  return r;
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_tile_sums(const Tin *in, int64_t n,
+                                                               int64_t *sums) {
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  int64_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i)
+    if (base + i < n) acc += (int64_t)in[base + i];
+  __shared__ int64_t tot;
+  block_excl_scan(acc, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_tile_apply(const Tin *in, int64_t n,
+                                                                const int64_t *tile_off,
+                                                                int64_t *out) {
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  int64_t v[SCAN_ITEMS];
+  int64_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    v[i] = (base + i < n) ? (int64_t)in[base + i] : 0;
+    acc += v[i];
+  }
+  __shared__ int64_t tot;
+  int64_t pre = block_excl_scan(acc, &tot) + (tile_off ? tile_off[blockIdx.x] : 0);
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    if (base + i < n) out[base + i] = pre;
+    pre += v[i];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == SCAN_THREADS - 1) out[n] = pre;
+}
+
+template <typename Tin>
+int exclusive_scan(const Tin *in, int64_t *out, int64_t n, cudaStream_t s) {
+  if (n <= 0) {
+    CPFIT_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
+    return CPFIT_OK;
+  }
+  int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  if (tiles == 1) {
+    scan_tile_apply<Tin><<<1, SCAN_THREADS, 0, s>>>(in, n, nullptr, out);
+    CPFIT_LAUNCH_CHECK("scan_tile_apply");
+    return CPFIT_OK;
+  }
+  Scratch<int64_t> sums(s), offs(s);
+  CPFIT_TRY(sums.alloc(tiles));
+  CPFIT_TRY(offs.alloc(tiles + 1));
+  scan_tile_sums<Tin><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, n, sums.ptr);
+  CPFIT_LAUNCH_CHECK("scan_tile_sums");
+  CPFIT_TRY(exclusive_scan<int64_t>(sums.ptr, offs.ptr, tiles, s));
+  scan_tile_apply<Tin><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, n, offs.ptr, out);
+  CPFIT_LAUNCH_CHECK("scan_tile_apply");
+  return CPFIT_OK;
+}
+
+template int exclusive_scan<int32_t>(const int32_t *, int64_t *, int64_t, cudaStream_t);
+template int exclusive_scan<int64_t>(const int64_t *, int64_t *, int64_t, cudaStream_t);
+template int exclusive_scan<uint32_t>(const uint32_t *, int64_t *, int64_t, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// simple element kernels
+
+__global__ void gather_i32_kernel(const int32_t *__restrict__ in,
+                                  const int32_t *__restrict__ idx,
+                                  int32_t *__restrict__ out, int64_t n) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = __ldg(in + __ldg(idx + k));
+}
+
+int gather_i32(const int32_t *in, const int32_t *idx, int32_t *out, int64_t n,
+               cudaStream_t s) {
+  if (n <= 0) return CPFIT_OK;
+  gather_i32_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(in, idx, out, n);
+  CPFIT_LAUNCH_CHECK("gather_i32");
+  return CPFIT_OK;
+}
+
+template <typename T>
+__global__ void gather_vals_kernel(const T *__restrict__ in, const int32_t *__restrict__ idx,
+                                   T *__restrict__ out, int64_t n) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = __ldg(in + __ldg(idx + k));
+}
+
+__global__ void iota_kernel(int32_t *out, int64_t n) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = (int32_t)k;
+}
+
+struct DelinParams {
+  int order;
+  uint64_t dims[CPFIT_MAXN];
+  int32_t *coords[CPFIT_MAXN];
+};
+
+// key -> coordinates, last mode fastest (core.py:93-102)
+__global__ void delinearize_kernel(const uint64_t *__restrict__ keys, int64_t n,
+                                   DelinParams p) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t rem = keys[e];
+#pragma unroll 1
+    for (int m = p.order - 1; m >= 0; --m) {
+      uint64_t d = p.dims[m];
+      uint64_t q = rem / d;
+      p.coords[m][e] = (int32_t)(rem - q * d);
+      rem = q;
+    }
+  }
+}
+
+// offsets[i] = first position whose (sorted) key >= i, for i in [0, dim]
+__global__ void offsets_from_sorted(const int32_t *__restrict__ sorted, int64_t n,
+                                    int64_t dim, int64_t *__restrict__ offsets) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t prev = e > 0 ? (int64_t)sorted[e - 1] : -1;
+    int64_t cur = e < n ? (int64_t)sorted[e] : dim;
+    for (int64_t i = prev + 1; i <= cur; ++i) offsets[i] = e;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// stable LSD radix sort of (key, position) pairs by 8-bit digits
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 8;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
+
+__global__ void __launch_bounds__(RS_THREADS)
+radix_upsweep(const int32_t *__restrict__ keys, int64_t n, int shift, int64_t nblocks,
+              int32_t *__restrict__ counts) {
+  __shared__ int hist[256];
+  for (int i = threadIdx.x; i < 256; i += RS_THREADS) hist[i] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * RS_TILE;
+  for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) {
+    int64_t k = base + i;
+    if (k < n) atomicAdd(&hist[((uint32_t)keys[k] >> shift) & 255u], 1);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < 256; d += RS_THREADS)
+    counts[(int64_t)d * nblocks + blockIdx.x] = hist[d];
+}
+
+// vals_in == nullptr means the identity (first pass).
+__global__ void __launch_bounds__(RS_THREADS)
+radix_downsweep(const int32_t *__restrict__ keys_in, const int32_t *__restrict__ vals_in,
+                int64_t n, int shift, int64_t nblocks, const int64_t *__restrict__ offs,
+                int32_t *__restrict__ keys_out, int32_t *__restrict__ vals_out) {
+  __shared__ int whist[RS_WARPS][257];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = lane; i < 257; i += 32) whist[w][i] = 0;
+  __syncwarp();
+  const int64_t wbase = (int64_t)blockIdx.x * RS_TILE + (int64_t)w * 32 * RS_ITEMS;
+  int32_t key[RS_ITEMS], rank[RS_ITEMS];
+  int digit[RS_ITEMS];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    int64_t k = wbase + j * 32 + lane;
+    bool valid = k < n;
+    key[j] = valid ? keys_in[k] : 0;
+    int d = valid ? (int)(((uint32_t)key[j] >> shift) & 255u) : 256;
+    digit[j] = d;
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    int pre = whist[w][d];
+    __syncwarp();
+    int leader = __ffs(peers) - 1;
+    if (lane == leader) whist[w][d] = pre + __popc(peers);
+    __syncwarp();
+    rank[j] = pre + __popc(peers & lt);
+  }
+  __syncthreads();
+  // exclusive scan over warps per digit
+  for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
+    int run = 0;
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) {
+      int c = whist[ww][d];
+      whist[ww][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    int64_t k = wbase + j * 32 + lane;
+    if (k < n) {
+      int d = digit[j];
+      int64_t pos = offs[(int64_t)d * nblocks + blockIdx.x] + whist[w][d] + rank[j];
+      keys_out[pos] = key[j];
+      vals_out[pos] = vals_in ? vals_in[k] : (int32_t)k;
+    }
+  }
+}
+
+// Stable sort of positions 0..n-1 by keys (non-negative, < dim).
+// Writes sorted keys and the permutation.
+static int radix_sort_positions(const int32_t *keys, int64_t n, int64_t dim,
+                                int32_t *sorted_keys, int32_t *perm, cudaStream_t s) {
+  int bits = 0;
+  while (bits < 31 && ((int64_t)1 << bits) < dim) ++bits;
+  int passes = (bits + 7) / 8;
+  if (passes == 0 || n <= 1) {
+    iota_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(perm, n);
+    CPFIT_LAUNCH_CHECK("iota");
+    if (n) CPFIT_CUDA(cudaMemcpyAsync(sorted_keys, keys, n * sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, s));
+    return CPFIT_OK;
+  }
+  int64_t nblocks = (n + RS_TILE - 1) / RS_TILE;
+  Scratch<int32_t> counts(s), k_tmp(s), v_tmp(s);
+  Scratch<int64_t> offs(s);
+  CPFIT_TRY(counts.alloc(256 * nblocks));
+  CPFIT_TRY(offs.alloc(256 * nblocks + 1));
+  CPFIT_TRY(k_tmp.alloc(n));
+  CPFIT_TRY(v_tmp.alloc(n));
+  // ping-pong so that the last pass lands in (sorted_keys, perm)
+  int32_t *kb[2], *vb[2];
+  if (passes % 2 == 1) {
+    kb[0] = sorted_keys; vb[0] = perm; kb[1] = k_tmp.ptr; vb[1] = v_tmp.ptr;
+  } else {
+    kb[0] = k_tmp.ptr; vb[0] = v_tmp.ptr; kb[1] = sorted_keys; vb[1] = perm;
+  }
+  const int32_t *kin = keys;
+  const int32_t *vin = nullptr;
+  for (int p = 0; p < passes; ++p) {
+    int shift = 8 * p;
+    radix_upsweep<<<(unsigned)nblocks, RS_THREADS, 0, s>>>(kin, n, shift, nblocks, counts.ptr);
+    CPFIT_LAUNCH_CHECK("radix_upsweep");
+    CPFIT_TRY(exclusive_scan<int32_t>(counts.ptr, offs.ptr, 256 * nblocks, s));
+    int32_t *ko = kb[p % 2], *vo = vb[p % 2];
+    radix_downsweep<<<(unsigned)nblocks, RS_THREADS, 0, s>>>(kin, vin, n, shift, nblocks,
+                                                             offs.ptr, ko, vo);
+    CPFIT_LAUNCH_CHECK("radix_downsweep");
+    kin = ko;
+    vin = vo;
+  }
+  return CPFIT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// task tables: every non-empty slice is cut into ceil(len / L) contiguous
+// tasks of near-equal length; slices with more than one task get partial
+// slots, combined in task order afterwards (deterministic, no atomics).
+
+__global__ void task_count_kernel(const int64_t *__restrict__ offsets, int64_t dim, int64_t L,
+                                  int32_t *__restrict__ nt, int32_t *__restrict__ nslot,
+                                  int32_t *__restrict__ split) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < dim;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t len = offsets[i + 1] - offsets[i];
+    int64_t t = (len + L - 1) / L;
+    nt[i] = (int32_t)t;
+    nslot[i] = t > 1 ? (int32_t)t : 0;
+    split[i] = t > 1 ? 1 : 0;
+  }
+}
+
+__global__ void task_fill_kernel(const int64_t *__restrict__ offsets, int64_t dim,
+                                 const int32_t *__restrict__ nt,
+                                 const int64_t *__restrict__ tstart,
+                                 const int64_t *__restrict__ sstart,
+                                 const int64_t *__restrict__ xstart, int64_t nnz,
+                                 int64_t *__restrict__ task_begin, int32_t *__restrict__ task_row,
+                                 int32_t *__restrict__ task_slot, int32_t *__restrict__ split_row,
+                                 int32_t *__restrict__ split_slot) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < dim;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = nt[i];
+    if (t == 0) continue;
+    int64_t len = offsets[i + 1] - offsets[i];
+    int64_t t0 = tstart[i];
+    for (int64_t j = 0; j < t; ++j) {
+      task_begin[t0 + j] = offsets[i] + (j * len) / t;
+      task_row[t0 + j] = (int32_t)i;
+      task_slot[t0 + j] = t > 1 ? (int32_t)(sstart[i] + j) : -1;
+    }
+    if (t > 1) {
+      int64_t x = xstart[i];
+      split_row[x] = (int32_t)i;
+      split_slot[x] = (int32_t)sstart[i];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    task_begin[tstart[dim]] = nnz;
+    split_slot[xstart[dim]] = (int32_t)sstart[dim];
+  }
+}
+
+static int build_tasks(CpfitModeLayout &L, int64_t dim, int64_t nnz, int64_t task_size,
+                       cudaStream_t s) {
+  Scratch<int32_t> nt(s), nslot(s), split(s);
+  Scratch<int64_t> tstart(s), sstart(s), xstart(s);
+  CPFIT_TRY(nt.alloc(dim));
+  CPFIT_TRY(nslot.alloc(dim));
+  CPFIT_TRY(split.alloc(dim));
+  CPFIT_TRY(tstart.alloc(dim + 1));
+  CPFIT_TRY(sstart.alloc(dim + 1));
+  CPFIT_TRY(xstart.alloc(dim + 1));
+  task_count_kernel<<<grid_for(dim, 256), 256, 0, s>>>(L.offsets, dim, task_size, nt.ptr,
+                                                       nslot.ptr, split.ptr);
+  CPFIT_LAUNCH_CHECK("task_count");
+  CPFIT_TRY(exclusive_scan<int32_t>(nt.ptr, tstart.ptr, dim, s));
+  CPFIT_TRY(exclusive_scan<int32_t>(nslot.ptr, sstart.ptr, dim, s));
+  CPFIT_TRY(exclusive_scan<int32_t>(split.ptr, xstart.ptr, dim, s));
+  int64_t tot[3];
+  CPFIT_CUDA(cudaMemcpyAsync(&tot[0], tstart.ptr + dim, 8, cudaMemcpyDeviceToHost, s));
+  CPFIT_CUDA(cudaMemcpyAsync(&tot[1], sstart.ptr + dim, 8, cudaMemcpyDeviceToHost, s));
+  CPFIT_CUDA(cudaMemcpyAsync(&tot[2], xstart.ptr + dim, 8, cudaMemcpyDeviceToHost, s));
+  CPFIT_CUDA(cudaStreamSynchronize(s));
+  L.ntasks = tot[0];
+  L.nslots = tot[1];
+  L.nsplit = tot[2];
+  L.task_size = task_size;
+  CPFIT_TRY(dalloc(&L.task_begin, L.ntasks + 1, s));
+  CPFIT_TRY(dalloc(&L.task_row, L.ntasks > 0 ? L.ntasks : 1, s));
+  CPFIT_TRY(dalloc(&L.task_slot, L.ntasks > 0 ? L.ntasks : 1, s));
+  CPFIT_TRY(dalloc(&L.split_row, L.nsplit > 0 ? L.nsplit : 1, s));
+  CPFIT_TRY(dalloc(&L.split_slot, L.nsplit + 1, s));
+  task_fill_kernel<<<grid_for(dim, 256), 256, 0, s>>>(
+      L.offsets, dim, nt.ptr, tstart.ptr, sstart.ptr, xstart.ptr, nnz, L.task_begin,
+      L.task_row, L.task_slot, L.split_row, L.split_slot);
+  CPFIT_LAUNCH_CHECK("task_fill");
+  return CPFIT_OK;
+}
+
+int ensure_layout(cpfit_pattern *p, int mode, cudaStream_t s) {
+  CpfitModeLayout &L = p->modes[mode];
+  if (L.built) return CPFIT_OK;
+  const int64_t n = p->nnz, dim = p->dims[mode];
+  CPFIT_TRY(dalloc(&L.offsets, dim + 1, s));
+  if (mode == 0) {
+    // keys are sorted, so mode 0 groups are already contiguous: perm = identity
+    L.perm = nullptr;
+    for (int k = 0; k < p->order; ++k) {
+      L.sorted_idx[k] = p->coords[k];
+      L.owns_sorted[k] = false;
+    }
+    if (n > 0) {
+      offsets_from_sorted<<<grid_for(n + 1, 256, 4), 256, 0, s>>>(p->coords[0], n, dim,
+                                                                  L.offsets);
+      CPFIT_LAUNCH_CHECK("offsets_from_sorted");
+    } else {
+      CPFIT_CUDA(cudaMemsetAsync(L.offsets, 0, (dim + 1) * sizeof(int64_t), s));
+    }
+  } else {
+    int32_t *sorted_keys = nullptr;
+    CPFIT_TRY(dalloc(&L.perm, n > 0 ? n : 1, s));
+    CPFIT_TRY(dalloc(&sorted_keys, n > 0 ? n : 1, s));
+    if (n > 0) {
+      CPFIT_TRY(radix_sort_positions(p->coords[mode], n, dim, sorted_keys, L.perm, s));
+      offsets_from_sorted<<<grid_for(n + 1, 256, 4), 256, 0, s>>>(sorted_keys, n, dim,
+                                                                  L.offsets);
+      CPFIT_LAUNCH_CHECK("offsets_from_sorted");
+    } else {
+      CPFIT_CUDA(cudaMemsetAsync(L.offsets, 0, (dim + 1) * sizeof(int64_t), s));
+    }
+    L.sorted_idx[mode] = sorted_keys;
+    L.owns_sorted[mode] = true;
+    for (int k = 0; k < p->order; ++k) {
+      if (k == mode) continue;
+      CPFIT_TRY(dalloc(&L.sorted_idx[k], n > 0 ? n : 1, s));
+      L.owns_sorted[k] = true;
+      CPFIT_TRY(gather_i32(p->coords[k], L.perm, L.sorted_idx[k], n, s));
+    }
+  }
+  CPFIT_TRY(build_tasks(L, dim, n, p->task_size, s));
+  L.built = true;
+  return CPFIT_OK;
+}
+
+template <typename T>
+static int permute_vals(const T *in, const int32_t *perm, T *out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return CPFIT_OK;
+  gather_vals_kernel<T><<<grid_for(n, 256, 4), 256, 0, s>>>(in, perm, out, n);
+  CPFIT_LAUNCH_CHECK("permute_values");
+  return CPFIT_OK;
+}
+
+}  // namespace cpfit
+
+using namespace cpfit;
+
+extern "C" {
+
+const char *cpfit_version(void) { return "cpfit-b200 0.1.0 (sm_100a)"; }
+
+const char *cpfit_last_error(void) { return g_err; }
+
+static int validate_dims(int order, const int64_t *dims) {
+  if (order < 1 || order > CPFIT_MAXN) {
+    set_error("order %d outside the supported range [1, %d]", order, CPFIT_MAXN);
+    return CPFIT_EINVAL;
+  }
+  for (int n = 0; n < order; ++n) {
+    if (dims[n] < 1 || dims[n] > INT32_MAX) {
+      set_error("dimension of mode %d (%lld) outside [1, 2^31-1]", n, (long long)dims[n]);
+      return CPFIT_EINVAL;
+    }
+  }
+  return CPFIT_OK;
+}
+
+int cpfit_pattern_create(int order, const int64_t *dims, int64_t nnz, const uint64_t *keys,
+                         void *stream, cpfit_pattern **out) {
+  *out = nullptr;
+  CPFIT_TRY(validate_dims(order, dims));
+  if (nnz < 0 || nnz > INT32_MAX) {
+    set_error("nnz %lld outside [0, 2^31-1]", (long long)nnz);
+    return CPFIT_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cpfit_pattern *p = new (std::nothrow) cpfit_pattern();
+  if (!p) return CPFIT_ENOMEM;
+  p->order = order;
+  p->nnz = nnz;
+  DelinParams dp;
+  dp.order = order;
+  for (int n = 0; n < order; ++n) {
+    p->dims[n] = dims[n];
+    dp.dims[n] = (uint64_t)dims[n];
+    int st = dalloc(&p->coords[n], nnz > 0 ? nnz : 1, s);
+    if (st) { cpfit_pattern_destroy(p); return st; }
+    dp.coords[n] = p->coords[n];
+  }
+  if (nnz > 0) {
+    delinearize_kernel<<<grid_for(nnz, 256, 4), 256, 0, s>>>(keys, nnz, dp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { cpfit_pattern_destroy(p); return cuda_status(e, "delinearize"); }
+  }
+  *out = p;
+  return CPFIT_OK;
+}
+
+int cpfit_pattern_create_coords(int order, const int64_t *dims, int64_t nnz,
+                                const int32_t *const *coords, void *stream,
+                                cpfit_pattern **out) {
+  *out = nullptr;
+  CPFIT_TRY(validate_dims(order, dims));
+  if (nnz < 0 || nnz > INT32_MAX) {
+    set_error("nnz %lld outside [0, 2^31-1]", (long long)nnz);
+    return CPFIT_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cpfit_pattern *p = new (std::nothrow) cpfit_pattern();
+  if (!p) return CPFIT_ENOMEM;
+  p->order = order;
+  p->nnz = nnz;
+  for (int n = 0; n < order; ++n) {
+    p->dims[n] = dims[n];
+    int st = dalloc(&p->coords[n], nnz > 0 ? nnz : 1, s);
+    if (st) { cpfit_pattern_destroy(p); return st; }
+    if (nnz > 0) {
+      cudaError_t e = cudaMemcpyAsync(p->coords[n], coords[n], nnz * sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) { cpfit_pattern_destroy(p); return cuda_status(e, "copy coords"); }
+    }
+  }
+  *out = p;
+  return CPFIT_OK;
+}
+
+int cpfit_pattern_destroy(cpfit_pattern *p) {
+  if (!p) return CPFIT_OK;
+  // stream-ordered frees on the legacy stream after a device sync keep this
+  // safe regardless of which stream last used the buffers
+  cudaDeviceSynchronize();
+  for (int m = 0; m < p->order; ++m) {
+    CpfitModeLayout &L = p->modes[m];
+    if (L.perm) cudaFree(L.perm);
+    if (L.offsets) cudaFree(L.offsets);
+    for (int k = 0; k < p->order; ++k)
+      if (L.owns_sorted[k] && L.sorted_idx[k]) cudaFree(L.sorted_idx[k]);
+    if (L.task_begin) cudaFree(L.task_begin);
+    if (L.task_row) cudaFree(L.task_row);
+    if (L.task_slot) cudaFree(L.task_slot);
+    if (L.split_row) cudaFree(L.split_row);
+    if (L.split_slot) cudaFree(L.split_slot);
+    if (L.identity_perm) cudaFree(L.identity_perm);
+  }
+  for (int n = 0; n < p->order; ++n)
+    if (p->coords[n]) cudaFree(p->coords[n]);
+  delete p;
+  return CPFIT_OK;
+}
+
+int cpfit_pattern_info(const cpfit_pattern *p, int *order, int64_t *nnz) {
+  if (!p) { set_error("null pattern"); return CPFIT_EINVAL; }
+  if (order) *order = p->order;
+  if (nnz) *nnz = p->nnz;
+  return CPFIT_OK;
+}
+
+int cpfit_pattern_coords(const cpfit_pattern *p, int mode, const int32_t **coords) {
+  if (!p || mode < 0 || mode >= p->order) {
+    set_error("mode %d out of range", mode);
+    return CPFIT_EINVAL;
+  }
+  *coords = p->coords[mode];
+  return CPFIT_OK;
+}
+
+int cpfit_pattern_set_task_size(cpfit_pattern *p, int64_t entries) {
+  if (!p || entries < 1) { set_error("task size must be >= 1"); return CPFIT_EINVAL; }
+  p->task_size = entries;
+  return CPFIT_OK;
+}
+
+int cpfit_pattern_mode_group(cpfit_pattern *p, int mode, void *stream, const int32_t **perm,
+                             const int64_t **offsets) {
+  if (!p || mode < 0 || mode >= p->order) {
+    set_error("mode %d out of range for order-%d tensor", mode, p ? p->order : 0);
+    return CPFIT_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CPFIT_TRY(ensure_layout(p, mode, s));
+  CpfitModeLayout &L = p->modes[mode];
+  if (perm) {
+    if (L.perm) {
+      *perm = L.perm;
+    } else {
+      if (!L.identity_perm) {
+        CPFIT_TRY(dalloc(&L.identity_perm, p->nnz > 0 ? p->nnz : 1, s));
+        iota_kernel<<<grid_for(p->nnz, 256, 4), 256, 0, s>>>(L.identity_perm, p->nnz);
+        CPFIT_LAUNCH_CHECK("iota");
+      }
+      *perm = L.identity_perm;
+    }
+  }
+  if (offsets) *offsets = L.offsets;
+  return CPFIT_OK;
+}
+
+int cpfit_pattern_mode_stats(cpfit_pattern *p, int mode, void *stream, int64_t *ntasks,
+                             int64_t *nsplit, int64_t *nslots) {
+  if (!p || mode < 0 || mode >= p->order) { set_error("bad mode"); return CPFIT_EINVAL; }
+  CPFIT_TRY(ensure_layout(p, mode, (cudaStream_t)stream));
+  const CpfitModeLayout &L = p->modes[mode];
+  if (ntasks) *ntasks = L.ntasks;
+  if (nsplit) *nsplit = L.nsplit;
+  if (nslots) *nslots = L.nslots;
+  return CPFIT_OK;
+}
+
+int cpfit_permute_values(cpfit_pattern *p, int mode, int dtype, const void *vals, void *out,
+                         void *stream) {
+  if (!p || mode < 0 || mode >= p->order) { set_error("bad mode"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  CPFIT_TRY(ensure_layout(p, mode, s));
+  CpfitModeLayout &L = p->modes[mode];
+  size_t es = dtype == CPFIT_F64 ? 8 : 4;
+  if (!L.perm) {
+    if (p->nnz) CPFIT_CUDA(cudaMemcpyAsync(out, vals, p->nnz * es, cudaMemcpyDeviceToDevice, s));
+    return CPFIT_OK;
+  }
+  if (dtype == CPFIT_F64)
+    return permute_vals((const double *)vals, L.perm, (double *)out, p->nnz, s);
+  if (dtype == CPFIT_F32)
+    return permute_vals((const float *)vals, L.perm, (float *)out, p->nnz, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+}  // extern "C"

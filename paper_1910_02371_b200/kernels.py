@@ -1,0 +1,219 @@
+"""All-at-once multi-tensor kernels on the B200: MTTKRP, TTTP/SDDMM, Gram and
+factor solves.
+
+Drop-in for the reference's kernels.py (same signatures, validation, error
+types and messages).  Each function validates on the host, then calls one
+hand-written sm_100a kernel of ``libcpfit_b200.so`` through the C-ABI
+(include/cpfit_b200.h) on the current torch CUDA stream.  There is no CPU
+fallback.
+
+Inputs: factor matrices may be numpy arrays (the reference's API: they are
+uploaded, results come back as numpy) or CUDA ``torch.Tensor`` (device
+resident; results stay on the device as tensors).  float32 CUDA factors select
+the fp32 kernels; everything else computes in float64 like the reference.
+
+Results are deterministic run to run (no floating-point atomics); ``threads``
+is accepted for signature compatibility and ignored, as the reference's
+results are thread-count independent too (kernels.py:12-15).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .core import SparseTensor, _dtype_code, cuda_device, current_stream
+from .exceptions import NumericalError
+from .validation import _is_torch, check_factor, check_factor_list, check_mode
+
+DEFAULT_TTTP_BUDGET_BYTES = 1 << 28
+DEFAULT_STAGE_ROWS = 256
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _compute_dtype(arrays):
+    """float32 only when every provided operand is a float32 CUDA tensor."""
+    torch = _torch()
+    provided = [a for a in arrays if a is not None]
+    if provided and all(_is_torch(a) and a.dtype == torch.float32 for a in provided):
+        return torch.float32
+    return torch.float64
+
+
+def _device_mode(arrays) -> bool:
+    return any(_is_torch(a) for a in arrays if a is not None)
+
+
+def _to_device(a, dtype):
+    torch = _torch()
+    if a is None:
+        return None
+    if _is_torch(a):
+        return a.to(device=cuda_device(), dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a)).to(cuda_device()).to(dtype)
+
+
+def _ptrs(tensors):
+    return _lib.ptr_array([0 if t is None else t.data_ptr() for t in tensors])
+
+
+def _vp(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(current_stream())
+
+
+# ---------------------------------------------------------------------------
+
+def mttkrp(t: SparseTensor, factors, mode: int, threads: int = 1):
+    """Matricized tensor times Khatri-Rao product (kernels.py:46-91).
+
+    out[i, r] = sum over entries with mode index i of value * prod over the
+    other modes of factor[i_n, r]; rows with no entries are exactly zero.
+    """
+    mode = check_mode(mode, t.order)
+    factors, rank = check_factor_list(factors, t.shape, skip_mode=mode)
+    dtype = _compute_dtype(factors)
+    on_device = _device_mode(factors)
+    torch = _torch()
+    dev = [_to_device(f, dtype) for f in factors]
+    out = torch.empty((t.shape[mode], rank), dtype=dtype, device=cuda_device())
+    if t.nnz == 0:
+        out.zero_()
+    else:
+        vals = t.sorted_values(mode, dtype)
+        _lib.check(_lib.load().cpfit_mttkrp(
+            t.device_pattern().handle, mode, _dtype_code(dtype), rank, _vp(vals), 1,
+            _ptrs(dev), _vp(out), _stream()), "mttkrp")
+    return out if on_device else out.cpu().numpy()
+
+
+def _tttp_slices(rank: int, h_slices, nnz: int, budget_bytes: int):
+    """kernels.py:94-102 (validation only: the fused kernel needs no slicing)."""
+    if h_slices is None:
+        per_slice = max(1, budget_bytes // max(1, nnz * 8))
+        h_slices = -(-rank // per_slice)
+    h_slices = int(h_slices)
+    if not 1 <= h_slices <= rank:
+        raise ValueError(f"h_slices must be in [1, rank], got {h_slices}")
+    return h_slices
+
+
+def tttp(t: SparseTensor, factors, h_slices: int | None = None,
+         budget_bytes: int = DEFAULT_TTTP_BUDGET_BYTES, threads: int = 1) -> SparseTensor:
+    """Tensor-times-tensor product (kernels.py:105-149).
+
+    out value at entry e = t value * sum_r prod over provided modes of
+    factors[n][coords[n][e], r]; None slots are skipped.  One fused pass:
+    ``h_slices`` is validated but no nnz x R intermediate ever exists.
+    """
+    factors, rank = check_factor_list(factors, t.shape, allow_missing=True)
+    if t.nnz == 0:
+        return t
+    _tttp_slices(rank, h_slices, t.nnz, budget_bytes)
+    dtype = _compute_dtype(factors)
+    torch = _torch()
+    dev = [_to_device(f, dtype) for f in factors]
+    vals = t.device_values(dtype)
+    out = torch.empty(t.nnz, dtype=dtype, device=cuda_device())
+    _lib.check(_lib.load().cpfit_tttp(
+        t.device_pattern().handle, _dtype_code(dtype), rank, _vp(vals), _ptrs(dev),
+        _vp(out), _stream()), "tttp")
+    return t.with_values(out)
+
+
+def sddmm(s: SparseTensor, u, v, threads: int = 1) -> SparseTensor:
+    """Sampled dense-dense matrix multiply (kernels.py:152-156)."""
+    if s.order != 2:
+        raise ValueError(f"sddmm requires an order-2 tensor, got order {s.order}")
+    return tttp(s, [u, v], threads=threads)
+
+
+def _weights_arg(weights: SparseTensor, mode: int, dtype):
+    return weights.sorted_values(mode, dtype)
+
+
+def gram_blocks(weights: SparseTensor, factors, mode: int, row_batches: int = 1,
+                stage_rows: int = DEFAULT_STAGE_ROWS, threads: int = 1):
+    """Per-row normal-equation matrices (kernels.py:159-212).
+
+    G[i] = sum over entries of row i of weight * h h^T, h = Hadamard product of
+    the other modes' factor rows.  ``row_batches`` / ``stage_rows`` are
+    validated memory knobs of the reference; the fused kernel needs neither.
+    """
+    mode = check_mode(mode, weights.order)
+    factors, rank = check_factor_list(factors, weights.shape, skip_mode=mode)
+    if not 1 <= row_batches:
+        raise ValueError("row_batches must be >= 1")
+    dtype = _compute_dtype(factors)
+    on_device = _device_mode(factors)
+    torch = _torch()
+    dev = [_to_device(f, dtype) for f in factors]
+    gram = torch.empty((weights.shape[mode], rank, rank), dtype=dtype, device=cuda_device())
+    if weights.nnz == 0:
+        gram.zero_()
+    else:
+        w = _weights_arg(weights, mode, dtype)
+        _lib.check(_lib.load().cpfit_gram(
+            weights.device_pattern().handle, mode, _dtype_code(dtype), rank, _vp(w), 1,
+            _ptrs(dev), _vp(gram), _stream()), "gram")
+    return gram if on_device else gram.cpu().numpy()
+
+
+def solve_factor(weights: SparseTensor, factors, rhs, mode: int, reg: float = 0.0,
+                 row_batches: int = 1, stage_rows: int = DEFAULT_STAGE_ROWS,
+                 threads: int = 1, return_gram: bool = False):
+    """Per-row regularised normal equations (kernels.py:215-267).
+
+    Solves (G_i + reg I) x_i = rhs_i for every row of ``mode``; empty rows
+    solve reg x = rhs (identity when reg == 0, which then requires rhs == 0).
+
+    Raises NumericalError naming the row on a singular system (reg == 0).
+    """
+    mode = check_mode(mode, weights.order)
+    rhs = check_factor(rhs, rows=weights.shape[mode], name="rhs")
+    rank = rhs.shape[1]
+    factors, frank = check_factor_list(factors, weights.shape, skip_mode=mode)
+    if not 1 <= row_batches:
+        raise ValueError("row_batches must be >= 1")
+    dtype = _compute_dtype(list(factors) + [rhs])
+    on_device = _device_mode(list(factors) + [rhs])
+    torch = _torch()
+    dev = [_to_device(f, dtype) for f in factors]
+    drhs = _to_device(rhs, dtype)
+    if frank != rank:
+        # the reference assembles G first, so negative weights win over this
+        if weights.nnz and bool((weights.device_values(dtype) < 0).any()):
+            raise ValueError("weights must be nonnegative for normal-equation assembly")
+        raise ValueError(f"rhs rank {rank} does not match factor rank {frank}")
+    reg = float(reg)
+    x = torch.empty((weights.shape[mode], rank), dtype=dtype, device=cuda_device())
+    gram = torch.empty((weights.shape[mode], rank, rank), dtype=dtype,
+                       device=cuda_device()) if return_gram else None
+    w = _weights_arg(weights, mode, dtype) if weights.nnz else None
+    bad = ctypes.c_int64(-1)
+    pat = weights.device_pattern() if weights.nnz or True else None
+    st = _lib.load().cpfit_solve_factor(
+        pat.handle, mode, _dtype_code(dtype), rank, _vp(w), 1, _ptrs(dev), _vp(drhs), reg,
+        _vp(x), _vp(gram), ctypes.byref(bad), _stream())
+    if st == _lib.EEMPTYROW:
+        raise NumericalError(f"mode {mode} row {bad.value}: no incident entries and reg=0 "
+                             "but right-hand side is nonzero")
+    if st == _lib.ESINGULAR:
+        raise NumericalError(f"mode {mode} row {bad.value}: singular normal equations "
+                             f"(reg={reg})")
+    _lib.check(st, "solve_factor")
+    if not on_device:
+        x = x.cpu().numpy()
+        gram = gram.cpu().numpy() if gram is not None else None
+    if return_gram:
+        return x, gram
+    return x
