@@ -134,6 +134,54 @@ int cpfit_solve_factor(cpfit_pattern *p, int mode, int dtype, int rank,
                        double reg, void *x_out, void *gram_out,
                        int64_t *bad_row, void *stream);
 
+/* TTTP with an affine epilogue: out[e] = alpha * m_e + beta * vals[e], with
+ * m_e = sum_r prod_n factors[n][i_n(e), r].  alpha = 2, beta = -2 gives the
+ * least-squares derivative tensor 2(m - t) (losses.py:41-48, model via
+ * model_at_observed = TTTP on the unit mask, losses.py:107-114); alpha = -1,
+ * beta = 1 the residual t - m (optim.py:250, 642-652). */
+int cpfit_tttp_axpby(cpfit_pattern *p, int dtype, int rank, const void *vals,
+                     const void *const *factors, double alpha, double beta,
+                     void *out, void *stream);
+
+/* ---- sampling (SparseTensor.sample, core.py:173-183) ------------------ */
+
+/* Keep entry e iff u_e < rate where u_e is draw (counter_offset + e) of
+ * numpy Generator(Philox(key)).random() -- bit-exact Philox4x64-10, so a
+ * shard with counter_offset = its first global entry reproduces the
+ * single-device sample.  *out is a new pattern holding the survivors in
+ * order; cpfit_pattern_parent_index gives their positions in `src`. */
+int cpfit_sample(cpfit_pattern *src, uint64_t key0, uint64_t key1,
+                 int64_t counter_offset, double rate, void *stream,
+                 cpfit_pattern **out);
+
+int cpfit_pattern_parent_index(const cpfit_pattern *p, const int32_t **idx);
+
+/* out[k] = in[idx[k]], k < n (values of sampled / permuted entries). */
+int cpfit_gather_values(int dtype, int64_t n, const int32_t *idx,
+                        const void *in, void *out, void *stream);
+
+/* ---- reductions and updates ------------------------------------------- */
+
+/* Deterministic (fixed-order) reductions in fp64, result copied to the host:
+ * op 0: sum x^2;  op 1: sum (x - y)^2;  op 2: sum x*y.
+ * Serves objective / rmse (losses.py:126-150, optim.py:642-652). */
+int cpfit_reduce(int op, int dtype, int64_t n, const void *x, const void *y,
+                 double *result, void *stream);
+
+/* SGD step out = (a - step*grad) - shrink*a in numpy's evaluation order
+ * (optim.py:313-330); *nonfinite = 1 if any result is not finite. */
+int cpfit_sgd_update(int dtype, int64_t n, const void *a, const void *grad,
+                     double step, double shrink, void *out, int *nonfinite,
+                     void *stream);
+
+/* One CCD++ column update of `mode` for rank-one column r (least squares,
+ * optim.py:249-268).  cols[q] = column r of factor q (contiguous, fp64);
+ * cols[mode] is ignored and `old_col` used instead; the updated column is
+ * written to new_col and the canonical-order residual updated in place. */
+int cpfit_ccd_update(cpfit_pattern *p, int mode, const double *const *cols,
+                     const double *old_col, double *new_col, double *resid,
+                     double reg, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,8 @@ SYMBOLS = (
     "cpfit_pattern_info", "cpfit_pattern_coords", "cpfit_pattern_set_task_size",
     "cpfit_pattern_mode_group", "cpfit_pattern_mode_stats", "cpfit_permute_values",
     "cpfit_tttp", "cpfit_mttkrp", "cpfit_gram", "cpfit_solve_factor",
+    "cpfit_tttp_axpby", "cpfit_sample", "cpfit_pattern_parent_index", "cpfit_gather_values",
+    "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_update",
 )
 
 _vp = ctypes.c_void_p
@@ -77,6 +79,16 @@ def load(path: str | None = None):
         "cpfit_gram": [_vp, _int, _int, _int, _vp, _int, _PP, _vp, _vp],
         "cpfit_solve_factor": [_vp, _int, _int, _int, _vp, _int, _PP, _vp, ctypes.c_double,
                                _vp, _vp, ctypes.POINTER(_i64), _vp],
+        "cpfit_tttp_axpby": [_vp, _int, _int, _vp, _PP, ctypes.c_double, ctypes.c_double,
+                             _vp, _vp],
+        "cpfit_sample": [_vp, ctypes.c_uint64, ctypes.c_uint64, _i64, ctypes.c_double, _vp,
+                         ctypes.POINTER(_vp)],
+        "cpfit_pattern_parent_index": [_vp, ctypes.POINTER(_vp)],
+        "cpfit_gather_values": [_int, _i64, _vp, _vp, _vp, _vp],
+        "cpfit_reduce": [_int, _int, _i64, _vp, _vp, ctypes.POINTER(ctypes.c_double), _vp],
+        "cpfit_sgd_update": [_int, _i64, _vp, _vp, ctypes.c_double, ctypes.c_double, _vp,
+                             ctypes.POINTER(_int), _vp],
+        "cpfit_ccd_update": [_vp, _int, _PP, _vp, _vp, _vp, ctypes.c_double, _vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

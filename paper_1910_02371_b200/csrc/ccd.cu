@@ -1,0 +1,173 @@
+// ccd.cu -- CCD++ single-column update for sm_100a.
+//
+// One (r, mode) step of the least-squares CCD++ sweep (optim.py:249-268):
+//   partial_e = prod_{p != mode} col_p[i_p(e)]         (p ascending)
+//   rho_e     = resid_e + partial_e * col_mode[i(e)]
+//   num_i = sum_{e in row i} rho_e partial_e, den_i = sum partial_e^2
+//   new_i = num_i / (den_i + reg) if den_i + reg > 0 else col_mode[i]
+//   resid_e = rho_e - partial_e * new[i(e)]
+// Pass A walks the mode-sorted tasks (warp per task, no atomics; split rows
+// combined in task order) and finalises new_i; pass B updates the residual
+// in canonical order (coalesced).  rho and resid use explicitly rounded
+// (non-contracted) operations so each element follows the reference's
+// rounding; only the per-row sums are reassociated.
+#include "common.cuh"
+
+namespace cpfit {
+
+struct CcdParams {
+  int order, mode;
+  int64_t nnz, dim;
+  const double *cols[CPFIT_MAXN];   // column r of every mode (contiguous, length I_n)
+  const int32_t *sidx[CPFIT_MAXN];  // mode-sorted coordinates (all modes)
+  const int32_t *coords[CPFIT_MAXN];
+  const int32_t *perm;              // sorted position -> entry (null: identity)
+  const int64_t *task_begin;
+  const int32_t *task_row;
+  const int32_t *task_slot;
+  int64_t ntasks;
+  const double *old_col;  // col_mode before the update
+  double *new_col;
+  double *slots;          // 2 * nslots (num, den)
+  double *resid;
+  double reg;
+};
+
+__device__ __forceinline__ double ccd_partial_sorted(const CcdParams &p, int64_t e) {
+  double part = 1.0;
+#pragma unroll
+  for (int q = 0; q < CPFIT_MAXN; ++q) {
+    if (q >= p.order) break;
+    if (q == p.mode) continue;
+    part = __dmul_rn(part, __ldg(p.cols[q] + __ldg(p.sidx[q] + e)));
+  }
+  return part;
+}
+
+__global__ void ccd_init_newcol(const CcdParams p) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.dim;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p.new_col[i] = p.reg > 0.0 ? 0.0 / p.reg : p.old_col[i];  // empty rows: num = den = 0
+}
+
+__global__ void __launch_bounds__(256) ccd_rows_kernel(const CcdParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < p.ntasks; t += nwarps) {
+    const int64_t b0 = p.task_begin[t], b1 = p.task_begin[t + 1];
+    const int64_t row = p.task_row[t];
+    const double oc = p.old_col[row];
+    double num = 0.0, den = 0.0;
+    for (int64_t e = b0 + lane; e < b1; e += 32) {
+      const double part = ccd_partial_sorted(p, e);
+      const int64_t ent = p.perm ? __ldg(p.perm + e) : e;
+      const double rho = __dadd_rn(p.resid[ent], __dmul_rn(part, oc));
+      num += __dmul_rn(rho, part);
+      den += __dmul_rn(part, part);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      num += __shfl_xor_sync(0xffffffffu, num, o);
+      den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    if (lane == 0) {
+      const int slot = p.task_slot[t];
+      if (slot < 0) {
+        const double dr = den + p.reg;
+        p.new_col[row] = dr > 0.0 ? num / dr : oc;
+      } else {
+        p.slots[2 * (int64_t)slot] = num;
+        p.slots[2 * (int64_t)slot + 1] = den;
+      }
+    }
+  }
+}
+
+__global__ void ccd_combine(const CcdParams p, const int32_t *__restrict__ split_row,
+                            const int32_t *__restrict__ split_slot, int64_t nsplit) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nsplit;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = split_row[s];
+    double num = 0.0, den = 0.0;
+    for (int64_t k = split_slot[s]; k < split_slot[s + 1]; ++k) {
+      num += p.slots[2 * k];
+      den += p.slots[2 * k + 1];
+    }
+    const double dr = den + p.reg;
+    p.new_col[row] = dr > 0.0 ? num / dr : p.old_col[row];
+  }
+}
+
+__global__ void ccd_resid_kernel(const CcdParams p) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < p.nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double part = 1.0;
+#pragma unroll
+    for (int q = 0; q < CPFIT_MAXN; ++q) {
+      if (q >= p.order) break;
+      if (q == p.mode) continue;
+      part = __dmul_rn(part, __ldg(p.cols[q] + __ldg(p.coords[q] + e)));
+    }
+    const int32_t i = __ldg(p.coords[p.mode] + e);
+    const double rho = __dadd_rn(p.resid[e], __dmul_rn(part, __ldg(p.old_col + i)));
+    p.resid[e] = __dsub_rn(rho, __dmul_rn(part, __ldg(p.new_col + i)));
+  }
+}
+
+}  // namespace cpfit
+
+using namespace cpfit;
+
+extern "C" {
+
+int cpfit_ccd_update(cpfit_pattern *pt, int mode, const double *const *cols,
+                     const double *old_col, double *new_col, double *resid, double reg,
+                     void *stream) {
+  if (!pt || mode < 0 || mode >= pt->order) {
+    set_error("mode %d out of range", mode);
+    return CPFIT_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CPFIT_TRY(ensure_layout(pt, mode, s));
+  CpfitModeLayout &L = pt->modes[mode];
+  CcdParams p{};
+  p.order = pt->order;
+  p.mode = mode;
+  p.nnz = pt->nnz;
+  p.dim = pt->dims[mode];
+  for (int q = 0; q < pt->order; ++q) {
+    p.cols[q] = q == mode ? old_col : cols[q];
+    p.sidx[q] = L.sorted_idx[q];
+    p.coords[q] = pt->coords[q];
+  }
+  p.perm = L.perm;
+  p.task_begin = L.task_begin;
+  p.task_row = L.task_row;
+  p.task_slot = L.task_slot;
+  p.ntasks = L.ntasks;
+  p.old_col = old_col;
+  p.new_col = new_col;
+  p.resid = resid;
+  p.reg = reg;
+  Scratch<double> slots(s);
+  if (L.nslots > 0) CPFIT_TRY(slots.alloc(2 * L.nslots));
+  p.slots = slots.ptr;
+  ccd_init_newcol<<<grid_for(p.dim, 256), 256, 0, s>>>(p);
+  CPFIT_LAUNCH_CHECK("ccd_init_newcol");
+  if (pt->nnz == 0) return CPFIT_OK;
+  int64_t blocks = (L.ntasks + 7) / 8;
+  int64_t cap = (int64_t)num_sms() * 8;
+  ccd_rows_kernel<<<(unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks)), 256, 0, s>>>(p);
+  CPFIT_LAUNCH_CHECK("ccd_rows");
+  if (L.nsplit > 0) {
+    ccd_combine<<<grid_for(L.nsplit, 128), 128, 0, s>>>(p, L.split_row, L.split_slot,
+                                                       L.nsplit);
+    CPFIT_LAUNCH_CHECK("ccd_combine");
+  }
+  ccd_resid_kernel<<<grid_for(pt->nnz, 256, 4), 256, 0, s>>>(p);
+  CPFIT_LAUNCH_CHECK("ccd_resid");
+  return CPFIT_OK;
+}
+
+}  // extern "C"

@@ -195,6 +195,7 @@ struct cpfit_pattern {
   int32_t *coords[CPFIT_MAXN] = {nullptr};
   int64_t task_size = 1024;
   CpfitModeLayout modes[CPFIT_MAXN];
+  int32_t *parent = nullptr;  // sampled patterns: entry -> entry of the source pattern
 };
 
 namespace cpfit {

@@ -554,6 +554,7 @@ int cpfit_pattern_destroy(cpfit_pattern *p) {
   }
   for (int n = 0; n < p->order; ++n)
     if (p->coords[n]) cudaFree(p->coords[n]);
+  if (p->parent) cudaFree(p->parent);
   delete p;
   return CPFIT_OK;
 }

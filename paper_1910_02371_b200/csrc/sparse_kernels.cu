@@ -30,6 +30,8 @@ struct TttpParams {
   const T *fac[CPFIT_MAXN];
   const T *vals;
   T *out;
+  int epi;        // 0: out = vals * acc;  1: out = alpha * acc + beta * vals
+  T alpha, beta;
 };
 
 template <typename T, int VEC, int LPE, int KV, int NP>
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(256) tttp_kernel(const TttpParams<T> p) {
       const T got = __shfl_sync(0xffffffffu, acc, (lane % G) * LPE);
       if (lane / G == s) result = got;
     }
-    if (valid) p.out[e] = my_val * result;
+    if (valid) p.out[e] = p.epi == 0 ? my_val * result : p.alpha * result + p.beta * my_val;
   }
 }
 
@@ -288,8 +290,12 @@ static int dispatch_mttkrp(const MttkrpParams<T> &p, int vec, cudaStream_t s) {
 
 template <typename T>
 static int run_tttp(cpfit_pattern *pt, int rank, const void *vals, const void *const *factors,
-                    void *out, cudaStream_t s) {
+                    void *out, cudaStream_t s, int epi = 0, double alpha = 0.0,
+                    double beta = 0.0) {
   TttpParams<T> p{};
+  p.epi = epi;
+  p.alpha = (T)alpha;
+  p.beta = (T)beta;
   p.rank = rank;
   p.nnz = pt->nnz;
   p.vals = (const T *)vals;
@@ -373,6 +379,18 @@ int cpfit_tttp(cpfit_pattern *p, int dtype, int rank, const void *vals,
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == CPFIT_F64) return run_tttp<double>(p, rank, vals, factors, out, s);
   if (dtype == CPFIT_F32) return run_tttp<float>(p, rank, vals, factors, out, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+int cpfit_tttp_axpby(cpfit_pattern *p, int dtype, int rank, const void *vals,
+                     const void *const *factors, double alpha, double beta, void *out,
+                     void *stream) {
+  if (!p) { set_error("null pattern"); return CPFIT_EINVAL; }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64) return run_tttp<double>(p, rank, vals, factors, out, s, 1, alpha, beta);
+  if (dtype == CPFIT_F32) return run_tttp<float>(p, rank, vals, factors, out, s, 1, alpha, beta);
   set_error("unknown dtype %d", dtype);
   return CPFIT_EINVAL;
 }
