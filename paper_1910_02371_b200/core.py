@@ -145,6 +145,7 @@ class _Shared:
     groups: dict = field(default_factory=dict)  # host (perm, offsets) per mode
     pattern: DevicePattern | None = None
     task_size: int | None = None
+    parent: object = None                # sampled patterns: positions in the source
 
 
 def _dtype_code(dtype) -> int:
