@@ -12,6 +12,7 @@ import concurrent.futures as cf
 import os
 import shutil
 import subprocess
+import zlib
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -21,7 +22,7 @@ LIB = os.path.join(HERE, "libcpfit_b200.so")
 INCLUDE = os.path.join(HERE, "..", "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+NVCC_FLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
 
@@ -47,7 +48,8 @@ def up_to_date() -> bool:
 
 
 def _compile(src: str, extra: list[str]) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
+    tag = ("_%08x" % zlib.crc32(" ".join(extra).encode())) if extra else ""
+    obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", tag + ".o"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= _deps_mtime():
         return obj
     cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-c", src, "-o", obj]
@@ -59,8 +61,10 @@ def _compile(src: str, extra: list[str]) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
+          lib: str | None = None) -> str:
+    lib = lib or LIB
+    if not force and lib == LIB and up_to_date():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     extra = list(extra or [])
@@ -68,13 +72,13 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
         extra += ["-Xptxas", "-v"]
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, extra), sources()))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

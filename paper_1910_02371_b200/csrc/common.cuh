@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/cpfit_b200.h"
@@ -121,12 +122,6 @@ __device__ __forceinline__ float shfl_xor(float v, int m) {
   return __shfl_xor_sync(0xffffffffu, v, m);
 }
 
-// Column-tiling of a rank-R row across a lane group: each of LPE lanes
-// handles KV vectors of VEC contiguous columns, columns (k*LPE + q)*VEC.
-struct RowTiling {
-  int vec, lpe, kv;
-};
-
 template <typename T>
 inline int pick_vec(int rank, const void *const *ptrs, int n) {
   size_t row_bytes = (size_t)rank * sizeof(T);
@@ -138,18 +133,6 @@ inline int pick_vec(int rank, const void *const *ptrs, int n) {
   for (int i = 0; i < n; ++i)
     if (ptrs[i] && ((uintptr_t)ptrs[i] % (vec * sizeof(T)) != 0)) vec = 1;
   return vec;
-}
-
-inline RowTiling pick_tiling(int rank, int vec, int kvmax) {
-  RowTiling t;
-  t.vec = vec;
-  int nv = (rank + vec - 1) / vec;  // vectors per row
-  int lpe = 4;
-  while (lpe < nv && lpe < 32) lpe *= 2;
-  t.lpe = lpe;
-  t.kv = (nv + lpe - 1) / lpe;
-  if (t.kv > kvmax) t.kv = -1;
-  return t;
 }
 
 // ---- device scan (exclusive, int64 out) -----------------------------------

@@ -1,0 +1,137 @@
+// sparse_api.cu -- C-ABI of TTTP / MTTKRP (kernels in sparse_kernels.cuh).
+//
+// Reference: kernels.tttp (kernels.py:105-149) / _jit.tttp3 (_jit.py:49-59);
+// kernels.mttkrp (kernels.py:46-91) / _jit.mttkrp3 (_jit.py:35-47).
+#include "sparse_kernels.cuh"
+
+namespace cpfit {
+
+extern template int dispatch_tttp<double>(const TttpParams<double> &, int, cudaStream_t);
+extern template int dispatch_tttp<float>(const TttpParams<float> &, int, cudaStream_t);
+extern template int dispatch_mttkrp<double>(const MttkrpParams<double> &, int, cudaStream_t);
+extern template int dispatch_mttkrp<float>(const MttkrpParams<float> &, int, cudaStream_t);
+
+template <typename T>
+static int run_tttp(cpfit_pattern *pt, int rank, const void *vals, const void *const *factors,
+                    void *out, cudaStream_t s, int epi = 0, double alpha = 0.0,
+                    double beta = 0.0) {
+  TttpParams<T> p{};
+  p.epi = epi;
+  p.alpha = (T)alpha;
+  p.beta = (T)beta;
+  p.rank = rank;
+  p.nnz = pt->nnz;
+  p.vals = (const T *)vals;
+  p.out = (T *)out;
+  int np = 0;
+  const void *ptrs[CPFIT_MAXN];
+  for (int n = 0; n < pt->order; ++n) {
+    if (!factors[n]) continue;
+    p.idx[np] = pt->coords[n];
+    p.fac[np] = (const T *)factors[n];
+    ptrs[np] = factors[n];
+    ++np;
+  }
+  if (np == 0) {
+    set_error("at least one factor matrix must be provided");
+    return CPFIT_EINVAL;
+  }
+  p.np = np;
+  if (pt->nnz == 0) return CPFIT_OK;
+  return dispatch_tttp<T>(p, pick_vec<T>(rank, ptrs, np), s);
+}
+
+template <typename T>
+static int run_mttkrp(cpfit_pattern *pt, int mode, int rank, const void *vals, int vals_sorted,
+                      const void *const *factors, void *out, cudaStream_t s) {
+  const int64_t dim = pt->dims[mode];
+  CPFIT_CUDA(cudaMemsetAsync(out, 0, (size_t)dim * rank * sizeof(T), s));
+  if (pt->nnz == 0) return CPFIT_OK;
+  CPFIT_TRY(ensure_layout(pt, mode, s));
+  CpfitModeLayout &L = pt->modes[mode];
+  MttkrpParams<T> p{};
+  p.rank = rank;
+  int np = 0;
+  const void *ptrs[CPFIT_MAXN];
+  for (int n = 0; n < pt->order; ++n) {
+    if (n == mode) continue;
+    if (!factors[n]) {
+      set_error("factor[%d] is required but missing", n);
+      return CPFIT_EINVAL;
+    }
+    p.idx[np] = L.sorted_idx[n];
+    p.fac[np] = (const T *)factors[n];
+    ptrs[np] = factors[n];
+    ++np;
+  }
+  p.np = np;
+  p.vals = (const T *)vals;
+  p.perm = vals_sorted ? nullptr : L.perm;
+  p.task_begin = L.task_begin;
+  p.task_row = L.task_row;
+  p.task_slot = L.task_slot;
+  p.ntasks = L.ntasks;
+  p.out = (T *)out;
+  Scratch<T> partial(s);
+  if (L.nslots > 0) CPFIT_TRY(partial.alloc((size_t)L.nslots * rank));
+  p.partial = partial.ptr;
+  if (np == 0) {
+    // order-1 tensor: out[i] = sum of values in row i (empty product = 1)
+    set_error("mttkrp needs an order >= 2 tensor");
+    return CPFIT_EINVAL;
+  }
+  CPFIT_TRY(dispatch_mttkrp<T>(p, pick_vec<T>(rank, ptrs, np), s));
+  if (L.nsplit > 0) {
+    combine_partials<T><<<grid_for(L.nsplit * 32, 256), 256, 0, s>>>(
+        L.split_row, L.split_slot, L.nsplit, rank, partial.ptr, (T *)out);
+    CPFIT_LAUNCH_CHECK("combine_partials");
+  }
+  return CPFIT_OK;
+}
+
+}  // namespace cpfit
+
+using namespace cpfit;
+
+extern "C" {
+
+int cpfit_tttp(cpfit_pattern *p, int dtype, int rank, const void *vals,
+               const void *const *factors, void *out, void *stream) {
+  if (!p) { set_error("null pattern"); return CPFIT_EINVAL; }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64) return run_tttp<double>(p, rank, vals, factors, out, s);
+  if (dtype == CPFIT_F32) return run_tttp<float>(p, rank, vals, factors, out, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+int cpfit_tttp_axpby(cpfit_pattern *p, int dtype, int rank, const void *vals,
+                     const void *const *factors, double alpha, double beta, void *out,
+                     void *stream) {
+  if (!p) { set_error("null pattern"); return CPFIT_EINVAL; }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64) return run_tttp<double>(p, rank, vals, factors, out, s, 1, alpha, beta);
+  if (dtype == CPFIT_F32) return run_tttp<float>(p, rank, vals, factors, out, s, 1, alpha, beta);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+int cpfit_mttkrp(cpfit_pattern *p, int mode, int dtype, int rank, const void *vals,
+                 int vals_sorted, const void *const *factors, void *out, void *stream) {
+  if (!p || mode < 0 || mode >= p->order) {
+    set_error("mode %d out of range for order-%d tensor", mode, p ? p->order : 0);
+    return CPFIT_EINVAL;
+  }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64)
+    return run_mttkrp<double>(p, mode, rank, vals, vals_sorted, factors, out, s);
+  if (dtype == CPFIT_F32)
+    return run_mttkrp<float>(p, mode, rank, vals, vals_sorted, factors, out, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+}  // extern "C"

@@ -1,0 +1,482 @@
+// sparse_kernels.cuh -- TTTP and segmented MTTKRP for sm_100a (templates;
+// instantiated per dtype in tttp_f64.cu, tttp_f32.cu, mttkrp_f64.cu,
+// mttkrp_f32.cu so nvcc compiles them in parallel).
+//
+// Both kernels are gather-bound: per nonzero they stream N int32 indices and
+// one value and gather N (TTTP) or N-1 (MTTKRP) factor rows of R values.
+// A lane group of LPE lanes owns one nonzero at a time and gathers each
+// factor row with 128-bit vector loads (one row = LPE lanes x 16 B, so a
+// fp64 R=16 row is one 128 B line fetched by 8 lanes); 32/LPE nonzeros are
+// in flight per warp instruction.  Indices and values are loaded coalesced,
+// one nonzero per lane, and broadcast to the owning group with shuffles.
+//
+// TTTP finishes the group sums with one transposed butterfly per batch.  MTTKRP walks the mode-sorted nonzeros task by task: a task is a
+// contiguous run of one output row (long rows are split into several tasks,
+// whose partial rows are combined in task order by a fix-up pass), so every
+// output element is produced by exactly one warp with a fixed summation
+// order: deterministic, no floating-point atomics.
+//
+// Reference: kernels.tttp (kernels.py:105-149) / _jit.tttp3 (_jit.py:49-59);
+// kernels.mttkrp (kernels.py:46-91) / _jit.mttkrp3 (_jit.py:35-47).
+#pragma once
+#include "common.cuh"
+
+// min resident 256-thread blocks per SM for the gather kernels (register cap)
+#ifndef CPFIT_SPARSE_MINB
+#define CPFIT_SPARSE_MINB 2
+#endif
+
+namespace cpfit {
+
+template <typename T>
+struct TttpParams {
+  int np;       // factors present (absent modes are dropped on the host)
+  int rank;
+  int64_t nnz;
+  const int32_t *idx[CPFIT_MAXN];
+  const T *fac[CPFIT_MAXN];
+  const T *vals;
+  T *out;
+  int epi;        // 0: out = vals * acc;  1: out = alpha * acc + beta * vals
+  T alpha, beta;
+};
+
+// Gather the factor rows of U consecutive nonzero slots (j = (s0+u)*G + g)
+// of the current 32-entry batch into registers.  Every load of the U entries
+// is issued before any is consumed (memory-level parallelism, no branches in
+// between).  `fq[n]` is the lane's base pointer (factor n + q*VEC), so a row
+// address is one 32-bit multiply + one wide add; column offsets are
+// immediates.  FULL: the tiling covers the rank exactly (no column predicate).
+template <typename T, int VEC, int LPE, int KV, int NPM, int U, bool FULL>
+__device__ __forceinline__ void gather_rows(const T *const (&fq)[NPM],
+                                            const int32_t (&my_idx)[NPM], int np,
+                                            unsigned rank, int s0, int g, int q,
+                                            T (&x)[U][NPM][KV][VEC]) {
+  constexpr int G = 32 / LPE;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int j = (s0 + u) * G + g;
+#pragma unroll
+    for (int n = 0; n < NPM; ++n) {
+      if (n >= np) break;
+      const unsigned row = (unsigned)__shfl_sync(0xffffffffu, my_idx[n], j);
+      const T *frow = reinterpret_cast<const T *>(reinterpret_cast<const char *>(fq[n]) +
+                                                  (unsigned long long)row * (rank * (unsigned)sizeof(T)));
+#pragma unroll
+      for (int k = 0; k < KV; ++k) {
+        if (FULL || (unsigned)((k * LPE + q) * VEC) < rank) {
+          load_vec<T, VEC>(frow + k * LPE * VEC, x[u][n][k]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) x[u][n][k][v] = T(0);
+        }
+      }
+    }
+  }
+}
+
+// Generic-order variant (any number of present modes): multiplies each row
+// into a running product instead of keeping every row in registers.
+template <typename T, int VEC, int LPE, int KV, int NPM>
+__device__ __forceinline__ void gather_product(const T *const (&fq)[NPM],
+                                               const int32_t (&my_idx)[NPM], int np,
+                                               unsigned rank, int s, int g, int q,
+                                               T (&prod)[KV][VEC]) {
+  constexpr int G = 32 / LPE;
+  const int j = s * G + g;
+#pragma unroll 1
+  for (int n = 0; n < np; ++n) {
+    int32_t mine = my_idx[0];
+#pragma unroll
+    for (int m = 1; m < NPM; ++m)
+      if (m == n) mine = my_idx[m];
+    const unsigned row = (unsigned)__shfl_sync(0xffffffffu, mine, j);
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      T x[VEC];
+      if ((unsigned)((k * LPE + q) * VEC) < rank) {
+        const T *base = nullptr;
+#pragma unroll
+        for (int m = 0; m < NPM; ++m)
+          if (m == n) base = fq[m];
+        load_vec<T, VEC>(base + (size_t)row * rank + k * LPE * VEC, x);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) x[v] = T(0);
+      }
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) prod[k][v] = n == 0 ? x[v] : prod[k][v] * x[v];
+    }
+  }
+}
+
+// TTTP: warp = 32 consecutive nonzeros, G = 32/LPE groups of LPE lanes.
+// Sub-iteration s gathers the rows of nonzero j = s*G + g into group g; every
+// lane accumulates its column slice's partial product-sum for each of the LPE
+// nonzeros its group visits (part[s]).  One transposed (reduce-scatter)
+// butterfly over the group then leaves lane q with the full sum of nonzero
+// q*G + g: LPE-1 shuffles per LPE nonzeros instead of log2(LPE)+1 per
+// nonzero.  Values and outputs are accessed in that permuted but coalesced
+// order.
+template <typename T, int VEC, int LPE, int KV, int NP, bool FULL>
+__global__ void __launch_bounds__(256, CPFIT_SPARSE_MINB) tttp_kernel(const TttpParams<T> p) {
+  constexpr int G = 32 / LPE;                      // nonzeros per warp step
+  constexpr int NPM = NP > 0 ? NP : CPFIT_MAXN;    // register slots for indices
+  constexpr int U = NP > 0 ? (LPE < 4 ? LPE : 4) : 1;
+  const int np = NP > 0 ? NP : p.np;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / LPE, q = lane % LPE;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * 32;
+  const unsigned rank = (unsigned)p.rank;
+  const T *fq[NPM];
+#pragma unroll
+  for (int n = 0; n < NPM; ++n) fq[n] = n < np ? p.fac[n] + q * VEC : nullptr;
+  const int my_slot = q * G + g;  // the nonzero of the batch this lane finishes
+
+  int32_t my_idx[NPM];
+  int64_t base = warp * 32;
+  {
+    const int64_t e = base + lane;
+    const bool ok = e < p.nnz;
+#pragma unroll
+    for (int n = 0; n < NPM; ++n) my_idx[n] = (n < np && ok) ? __ldg(p.idx[n] + e) : 0;
+  }
+  for (; base < p.nnz; base += stride) {
+    // prefetch the next batch's indices (software pipelining)
+    int32_t nx_idx[NPM];
+    {
+      const int64_t e = base + stride + lane;
+      const bool ok = e < p.nnz;
+#pragma unroll
+      for (int n = 0; n < NPM; ++n) nx_idx[n] = (n < np && ok) ? __ldg(p.idx[n] + e) : 0;
+    }
+    const int64_t eo = base + my_slot;
+    const bool out_ok = eo < p.nnz;
+    const T my_val = out_ok ? __ldg(p.vals + eo) : T(0);
+    T part[LPE];
+    if constexpr (NP > 0) {
+#pragma unroll
+      for (int s0 = 0; s0 < LPE; s0 += U) {
+        T x[U][NPM][KV][VEC];
+        gather_rows<T, VEC, LPE, KV, NPM, U, FULL>(fq, my_idx, np, rank, s0, g, q, x);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          T acc = T(0);
+#pragma unroll
+          for (int k = 0; k < KV; ++k)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              T prod = x[u][0][k][v];
+#pragma unroll
+              for (int n = 1; n < NPM; ++n) prod = prod * x[u][n][k][v];
+              acc += prod;
+            }
+          part[s0 + u] = acc;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < LPE; ++s) {
+        T prod[KV][VEC];
+        gather_product<T, VEC, LPE, KV, NPM>(fq, my_idx, np, rank, s, g, q, prod);
+        T acc = T(0);
+#pragma unroll
+        for (int k = 0; k < KV; ++k)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc += prod[k][v];
+        part[s] = acc;
+      }
+    }
+    // reduce-scatter over the LPE lanes of the group: lane q ends with the
+    // total of nonzero s = q (fixed butterfly order: deterministic)
+#pragma unroll
+    for (int half = LPE / 2; half > 0; half >>= 1) {
+      const bool upper = (q & half) != 0;
+#pragma unroll
+      for (int i = 0; i < half; ++i) {
+        const T keep = upper ? part[half + i] : part[i];
+        const T send = upper ? part[i] : part[half + i];
+        part[i] = keep + shfl_xor(send, half);
+      }
+    }
+    if (out_ok)
+      p.out[eo] = p.epi == 0 ? my_val * part[0] : p.alpha * part[0] + p.beta * my_val;
+#pragma unroll
+    for (int n = 0; n < NPM; ++n) my_idx[n] = nx_idx[n];
+  }
+}
+
+template <typename T>
+struct MttkrpParams {
+  int np;  // other modes
+  int rank;
+  const int32_t *idx[CPFIT_MAXN];  // mode-sorted coordinates of the other modes
+  const T *fac[CPFIT_MAXN];
+  const T *vals;          // canonical order if perm != null, else mode-sorted
+  const int32_t *perm;    // mode-sorted position -> canonical entry
+  const int64_t *task_begin;
+  const int32_t *task_row;
+  const int32_t *task_slot;
+  int64_t ntasks;
+  T *out;
+  T *partial;
+};
+
+// One batch of up to 32 entries: coalesced indices (row 0 and value 0 past
+// the end, so padded slots contribute exactly nothing) and values.
+template <typename T, int NPM>
+__device__ __forceinline__ void mttkrp_load_batch(const MttkrpParams<T> &p, int np, int64_t e,
+                                                  int64_t end, int32_t (&ix)[NPM], T &v) {
+  const bool ok = e < end;
+#pragma unroll
+  for (int n = 0; n < NPM; ++n) ix[n] = (n < np && ok) ? __ldg(p.idx[n] + e) : 0;
+  v = T(0);
+  if (ok) v = p.perm ? __ldg(p.vals + __ldg(p.perm + e)) : __ldg(p.vals + e);
+}
+
+template <typename T, int VEC, int LPE, int KV, int NP, bool FULL>
+__global__ void __launch_bounds__(256, CPFIT_SPARSE_MINB) mttkrp_kernel(const MttkrpParams<T> p) {
+  constexpr int G = 32 / LPE;
+  constexpr int NPM = NP > 0 ? NP : CPFIT_MAXN;
+  constexpr int U = NP > 0 ? (LPE < 4 ? LPE : 4) : 1;
+  const int np = NP > 0 ? NP : p.np;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / LPE, q = lane % LPE;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned rank = (unsigned)p.rank;
+  const T *fq[NPM];
+#pragma unroll
+  for (int n = 0; n < NPM; ++n) fq[n] = n < np ? p.fac[n] + q * VEC : nullptr;
+
+  for (int64_t t = warp; t < p.ntasks; t += nwarps) {
+    const int64_t b0 = p.task_begin[t], b1 = p.task_begin[t + 1];
+    T acc[KV][VEC];
+#pragma unroll
+    for (int k = 0; k < KV; ++k)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[k][v] = T(0);
+
+    int32_t my_idx[NPM];
+    T my_val;
+    mttkrp_load_batch<T, NPM>(p, np, b0 + lane, b1, my_idx, my_val);
+    for (int64_t base = b0; base < b1; base += 32) {
+      int32_t nx_idx[NPM];
+      T nx_val;
+      mttkrp_load_batch<T, NPM>(p, np, base + 32 + lane, b1, nx_idx, nx_val);
+      const int cnt = (int)(b1 - base < 32 ? b1 - base : 32);
+#pragma unroll
+      for (int s0 = 0; s0 < LPE; s0 += U) {
+        if (s0 * G >= cnt) break;  // warp-uniform: the rest of the batch is empty
+        if constexpr (NP > 0) {
+          T x[U][NPM][KV][VEC];
+          gather_rows<T, VEC, LPE, KV, NPM, U, FULL>(fq, my_idx, np, rank, s0, g, q, x);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const T v = __shfl_sync(0xffffffffu, my_val, (s0 + u) * G + g);
+#pragma unroll
+            for (int k = 0; k < KV; ++k)
+#pragma unroll
+              for (int w = 0; w < VEC; ++w) {
+                T prod = x[u][0][k][w];
+#pragma unroll
+                for (int n = 1; n < NPM; ++n) prod = prod * x[u][n][k][w];
+                acc[k][w] += prod * v;
+              }
+          }
+        } else {
+          T prod[KV][VEC];
+          gather_product<T, VEC, LPE, KV, NPM>(fq, my_idx, np, rank, s0, g, q, prod);
+          const T v = __shfl_sync(0xffffffffu, my_val, s0 * G + g);
+#pragma unroll
+          for (int k = 0; k < KV; ++k)
+#pragma unroll
+            for (int w = 0; w < VEC; ++w) acc[k][w] += prod[k][w] * v;
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < NPM; ++n) my_idx[n] = nx_idx[n];
+      my_val = nx_val;
+    }
+    // combine the G groups (fixed tree order)
+#pragma unroll
+    for (int o = LPE; o < 32; o <<= 1)
+#pragma unroll
+      for (int k = 0; k < KV; ++k)
+#pragma unroll
+        for (int w = 0; w < VEC; ++w) acc[k][w] += shfl_xor(acc[k][w], o);
+    if (g == 0) {
+      const int slot = p.task_slot[t];
+      T *dst = slot < 0 ? p.out + (int64_t)p.task_row[t] * rank
+                        : p.partial + (int64_t)slot * rank;
+#pragma unroll
+      for (int k = 0; k < KV; ++k) {
+        const int col = (k * LPE + q) * VEC;
+        if (FULL || col < (int)rank) store_vec<T, VEC>(dst + col, acc[k]);
+      }
+    }
+  }
+}
+
+// Sum the partial rows of split slices in task order.
+template <typename T>
+__global__ void combine_partials(const int32_t *__restrict__ split_row,
+                                 const int32_t *__restrict__ split_slot, int64_t nsplit,
+                                 int rank, const T *__restrict__ partial, T *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < nsplit; s += nwarps) {
+    const int64_t row = split_row[s];
+    const int64_t a = split_slot[s], b = split_slot[s + 1];
+    for (int c = lane; c < rank; c += 32) {
+      T acc = partial[a * rank + c];
+      for (int64_t k = a + 1; k < b; ++k) acc += partial[k * rank + c];
+      out[row * rank + c] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launch + lane-tiling dispatch (instantiated per dtype in tttp_f64.cu, ...)
+
+template <typename T, int VEC, int LPE, int KV>
+static int launch_tttp_np(const TttpParams<T> &p, cudaStream_t s) {
+  const unsigned grid = grid_for((p.nnz + 31) / 32 * 32, 256);
+  const bool full = p.rank == LPE * VEC * KV;
+  constexpr bool HOT = (sizeof(T) == 8 && VEC == 2) || (sizeof(T) == 4 && VEC == 4);
+  if constexpr (HOT) {
+    if (p.np == 3 && full) {
+      tttp_kernel<T, VEC, LPE, KV, 3, true><<<grid, 256, 0, s>>>(p);
+      CPFIT_LAUNCH_CHECK("tttp_kernel");
+      return CPFIT_OK;
+    }
+    if (p.np == 4 && full) {
+      tttp_kernel<T, VEC, LPE, KV, 4, true><<<grid, 256, 0, s>>>(p);
+      CPFIT_LAUNCH_CHECK("tttp_kernel");
+      return CPFIT_OK;
+    }
+    if (p.np == 3) {  // ranks the lane tiling does not cover exactly (e.g. R = 10)
+      tttp_kernel<T, VEC, LPE, KV, 3, false><<<grid, 256, 0, s>>>(p);
+      CPFIT_LAUNCH_CHECK("tttp_kernel");
+      return CPFIT_OK;
+    }
+  }
+  tttp_kernel<T, VEC, LPE, KV, 0, false><<<grid, 256, 0, s>>>(p);
+  CPFIT_LAUNCH_CHECK("tttp_kernel");
+  return CPFIT_OK;
+}
+
+template <typename T, int VEC, int LPE, int KV>
+static int launch_mttkrp_np(const MttkrpParams<T> &p, cudaStream_t s) {
+  int64_t blocks = (p.ntasks + 7) / 8;
+  int64_t cap = (int64_t)num_sms() * 8;
+  const unsigned grid = (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+  const bool full = p.rank == LPE * VEC * KV;
+  constexpr bool HOT = (sizeof(T) == 8 && VEC == 2) || (sizeof(T) == 4 && VEC == 4);
+  if constexpr (HOT) {
+    if (p.np == 2 && full) {
+      mttkrp_kernel<T, VEC, LPE, KV, 2, true><<<grid, 256, 0, s>>>(p);
+      CPFIT_LAUNCH_CHECK("mttkrp_kernel");
+      return CPFIT_OK;
+    }
+    if (p.np == 3 && full) {
+      mttkrp_kernel<T, VEC, LPE, KV, 3, true><<<grid, 256, 0, s>>>(p);
+      CPFIT_LAUNCH_CHECK("mttkrp_kernel");
+      return CPFIT_OK;
+    }
+    if (p.np == 2) {  // ranks the lane tiling does not cover exactly (e.g. R = 10)
+      mttkrp_kernel<T, VEC, LPE, KV, 2, false><<<grid, 256, 0, s>>>(p);
+      CPFIT_LAUNCH_CHECK("mttkrp_kernel");
+      return CPFIT_OK;
+    }
+  }
+  mttkrp_kernel<T, VEC, LPE, KV, 0, false><<<grid, 256, 0, s>>>(p);
+  CPFIT_LAUNCH_CHECK("mttkrp_kernel");
+  return CPFIT_OK;
+}
+
+// Tiling policies (tools/tiling_sweep.py, profiles/r1_tiling_sweep.md):
+//  TTTP   -- 8 lanes per nonzero (LPE = 8, fewer when the row is narrower),
+//            KV = ceil(nv / 8) vectors per lane.
+//  MTTKRP -- fp64: 2 vectors per lane; fp32: 1 vector per lane.
+// (lpe, kv) pairs outside the instantiated set fall back to LPE = 32.
+template <typename F>
+static int tttp_tiling_dispatch(int nv, F &&f) {
+  if (nv <= 1) return f.template operator()<1, 1>();
+  if (nv <= 2) return f.template operator()<2, 1>();
+  if (nv <= 4) return f.template operator()<4, 1>();
+  if (nv <= 8) return f.template operator()<8, 1>();
+  if (nv <= 16) return f.template operator()<8, 2>();
+  if (nv <= 32) return f.template operator()<8, 4>();
+  if (nv <= 64) return f.template operator()<8, 8>();
+  if (nv <= 128) return f.template operator()<16, 8>();
+  if (nv <= 256) return f.template operator()<32, 8>();
+  set_error("rank too large for the TTTP kernel (%d vectors per row)", nv);
+  return CPFIT_EINVAL;
+}
+
+template <int KVT, typename F>
+static int mttkrp_tiling_dispatch(int nv, F &&f) {
+  if constexpr (KVT == 2) {
+    if (nv <= 1) return f.template operator()<1, 1>();
+    if (nv <= 2) return f.template operator()<1, 2>();
+    if (nv <= 4) return f.template operator()<2, 2>();
+    if (nv <= 8) return f.template operator()<4, 2>();
+    if (nv <= 16) return f.template operator()<8, 2>();
+    if (nv <= 32) return f.template operator()<16, 2>();
+  } else {
+    if (nv <= 1) return f.template operator()<1, 1>();
+    if (nv <= 2) return f.template operator()<2, 1>();
+    if (nv <= 4) return f.template operator()<4, 1>();
+    if (nv <= 8) return f.template operator()<8, 1>();
+    if (nv <= 16) return f.template operator()<16, 1>();
+    if (nv <= 32) return f.template operator()<32, 1>();
+  }
+  if (nv <= 64) return f.template operator()<32, 2>();
+  if (nv <= 128) return f.template operator()<32, 4>();
+  if (nv <= 256) return f.template operator()<32, 8>();
+  set_error("rank too large for the MTTKRP kernel (%d vectors per row)", nv);
+  return CPFIT_EINVAL;
+}
+
+template <typename T>
+int dispatch_tttp(const TttpParams<T> &p, int vec, cudaStream_t s) {
+  const int nv = (p.rank + vec - 1) / vec;
+  if constexpr (sizeof(T) == 8) {
+    if (vec == 2)
+      return tttp_tiling_dispatch(nv, [&]<int L, int K>() { return launch_tttp_np<T, 2, L, K>(p, s); });
+    return tttp_tiling_dispatch(nv, [&]<int L, int K>() { return launch_tttp_np<T, 1, L, K>(p, s); });
+  } else {
+    if (vec == 4)
+      return tttp_tiling_dispatch(nv, [&]<int L, int K>() { return launch_tttp_np<T, 4, L, K>(p, s); });
+    if (vec == 2)
+      return tttp_tiling_dispatch(nv, [&]<int L, int K>() { return launch_tttp_np<T, 2, L, K>(p, s); });
+    return tttp_tiling_dispatch(nv, [&]<int L, int K>() { return launch_tttp_np<T, 1, L, K>(p, s); });
+  }
+}
+
+template <typename T>
+int dispatch_mttkrp(const MttkrpParams<T> &p, int vec, cudaStream_t s) {
+  const int nv = (p.rank + vec - 1) / vec;
+  constexpr int KVT = sizeof(T) == 8 ? 2 : 1;
+  if constexpr (sizeof(T) == 8) {
+    if (vec == 2)
+      return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 2, L, K>(p, s); });
+    return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 1, L, K>(p, s); });
+  } else {
+    if (vec == 4)
+      return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 4, L, K>(p, s); });
+    if (vec == 2)
+      return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 2, L, K>(p, s); });
+    return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 1, L, K>(p, s); });
+  }
+}
+
+template <typename T>
+int dispatch_tttp(const TttpParams<T> &p, int vec, cudaStream_t s);
+template <typename T>
+int dispatch_mttkrp(const MttkrpParams<T> &p, int vec, cudaStream_t s);
+
+}  // namespace cpfit
