@@ -43,6 +43,10 @@ R = 16
 NNZ = 10_000_000
 
 
+def num_sms_probe(torch):
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -332,6 +336,44 @@ def main():
                 "unit": "GB/s", "frac": kernels[dom]["gbs"] / peak, "peak_kind": peak_kind,
                 "traffic": None,
                 "byte_model": "gather-inclusive algorithmic bytes, SURVEY.md 8(d)"}
+    # gather ceiling: the same row gathers with no compute (probe kernel)
+    probe = None
+    try:
+        pout = torch.empty(num_sms_probe(torch) * 256 * 4, dtype=torch.float64, device=dev)
+        coords = [pat.coords(n) for n in range(3)]
+        L0 = pat.mode_group(0)  # noqa: F841  (mode-0 order == canonical)
+
+        def run_probe(streams):
+            arr = _lib.ptr_array([c.data_ptr() for c in streams])
+            _lib.check(L.cpfit_probe_gather(ctypes.c_void_p(dfs[0].data_ptr()), R * 8,
+                                            len(streams), arr, t.nnz,
+                                            ctypes.c_void_p(pout.data_ptr()), pout.numel(), sp))
+        for _ in range(3):
+            run_probe(coords)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(10):
+            run_probe(coords)
+        b.record(stream)
+        torch.cuda.synchronize()
+        p3 = a.elapsed_time(b) / 10
+        a.record(stream)
+        for _ in range(10):
+            run_probe(coords[1:])
+        b.record(stream)
+        torch.cuda.synchronize()
+        p2 = a.elapsed_time(b) / 10
+        probe = {"ms_3rows": p3, "ms_2rows": p2,
+                 "gather_gbs_3rows": t.nnz * 3 * R * 8 / (p3 * 1e-3) / 1e9,
+                 "gather_gbs_2rows": t.nnz * 2 * R * 8 / (p2 * 1e-3) / 1e9,
+                 "what": "cpfit_probe_gather: the kernels' row gathers (same indices, "
+                         "128 B rows, L2-resident table) with no shuffles/compute"}
+        kernels["tttp"]["frac_of_gather_ceiling"] = p3 / kernels["tttp"]["ms"]
+        for m in range(3):
+            kernels[f"mttkrp{m}"]["frac_of_gather_ceiling"] = p2 / kernels[f"mttkrp{m}"]["ms"]
+        roofline["frac_of_gather_ceiling"] = kernels[dom]["frac_of_gather_ceiling"]
+    except Exception as exc:  # the probe is informational
+        probe = {"error": str(exc)}
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
@@ -374,7 +416,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE cfg 2 shape/value laws)",
             "config": dict(CONFIG, parallelism=f"nnz-shard{world}" if world > 1 else "1gpu"),
-            "roofline": roofline, "kernels": kernels,
+            "roofline": roofline, "kernels": kernels, "gather_ceiling": probe,
             "compulsory_bytes_per_pass": compulsory,
             "clocks": clk, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
         }

@@ -34,7 +34,7 @@ SYMBOLS = (
     "cpfit_pattern_mode_group", "cpfit_pattern_mode_stats", "cpfit_permute_values",
     "cpfit_tttp", "cpfit_mttkrp", "cpfit_gram", "cpfit_solve_factor",
     "cpfit_tttp_axpby", "cpfit_sample", "cpfit_pattern_parent_index", "cpfit_gather_values",
-    "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_update",
+    "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_update", "cpfit_probe_gather",
 )
 
 _vp = ctypes.c_void_p
@@ -89,6 +89,7 @@ def load(path: str | None = None):
         "cpfit_sgd_update": [_int, _i64, _vp, _vp, ctypes.c_double, ctypes.c_double, _vp,
                              ctypes.POINTER(_int), _vp],
         "cpfit_ccd_update": [_vp, _int, _PP, _vp, _vp, _vp, ctypes.c_double, _vp],
+        "cpfit_probe_gather": [_vp, _int, _int, _PP, _i64, _vp, _i64, _vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
