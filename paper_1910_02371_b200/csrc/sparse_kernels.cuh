@@ -21,9 +21,16 @@
 #pragma once
 #include "common.cuh"
 
-// min resident 256-thread blocks per SM for the gather kernels (register cap)
-#ifndef CPFIT_SPARSE_MINB
-#define CPFIT_SPARSE_MINB 2
+// Min resident 256-thread blocks per SM (register cap) and the fp64 MTTKRP
+// lane tiling, tuned on B200 with tools/tiling_sweep.py (profiles/r1_tuning.md).
+#ifndef CPFIT_TTTP_MINB
+#define CPFIT_TTTP_MINB 2
+#endif
+#ifndef CPFIT_MTTKRP_MINB
+#define CPFIT_MTTKRP_MINB 3
+#endif
+#ifndef CPFIT_MTTKRP_KVT64
+#define CPFIT_MTTKRP_KVT64 1
 #endif
 
 namespace cpfit {
@@ -119,7 +126,7 @@ __device__ __forceinline__ void gather_product(const T *const (&fq)[NPM],
 // nonzero.  Values and outputs are accessed in that permuted but coalesced
 // order.
 template <typename T, int VEC, int LPE, int KV, int NP, bool FULL>
-__global__ void __launch_bounds__(256, CPFIT_SPARSE_MINB) tttp_kernel(const TttpParams<T> p) {
+__global__ void __launch_bounds__(256, CPFIT_TTTP_MINB) tttp_kernel(const TttpParams<T> p) {
   constexpr int G = 32 / LPE;                      // nonzeros per warp step
   constexpr int NPM = NP > 0 ? NP : CPFIT_MAXN;    // register slots for indices
   constexpr int U = NP > 0 ? (LPE < 4 ? LPE : 4) : 1;
@@ -236,7 +243,7 @@ __device__ __forceinline__ void mttkrp_load_batch(const MttkrpParams<T> &p, int 
 }
 
 template <typename T, int VEC, int LPE, int KV, int NP, bool FULL>
-__global__ void __launch_bounds__(256, CPFIT_SPARSE_MINB) mttkrp_kernel(const MttkrpParams<T> p) {
+__global__ void __launch_bounds__(256, CPFIT_MTTKRP_MINB) mttkrp_kernel(const MttkrpParams<T> p) {
   constexpr int G = 32 / LPE;
   constexpr int NPM = NP > 0 ? NP : CPFIT_MAXN;
   constexpr int U = NP > 0 ? (LPE < 4 ? LPE : 4) : 1;
@@ -250,8 +257,15 @@ __global__ void __launch_bounds__(256, CPFIT_SPARSE_MINB) mttkrp_kernel(const Mt
 #pragma unroll
   for (int n = 0; n < NPM; ++n) fq[n] = n < np ? p.fac[n] + q * VEC : nullptr;
 
+  // persistent warps: boundaries of the next task are fetched one task ahead
+  int64_t nb0 = warp < p.ntasks ? p.task_begin[warp] : 0;
+  int64_t nb1 = warp < p.ntasks ? p.task_begin[warp + 1] : 0;
   for (int64_t t = warp; t < p.ntasks; t += nwarps) {
-    const int64_t b0 = p.task_begin[t], b1 = p.task_begin[t + 1];
+    const int64_t b0 = nb0, b1 = nb1;
+    if (t + nwarps < p.ntasks) {
+      nb0 = p.task_begin[t + nwarps];
+      nb1 = p.task_begin[t + nwarps + 1];
+    }
     T acc[KV][VEC];
 #pragma unroll
     for (int k = 0; k < KV; ++k)
@@ -370,8 +384,9 @@ static int launch_tttp_np(const TttpParams<T> &p, cudaStream_t s) {
 
 template <typename T, int VEC, int LPE, int KV>
 static int launch_mttkrp_np(const MttkrpParams<T> &p, cudaStream_t s) {
+  // persistent grid: exactly the resident capacity (no partial waves)
   int64_t blocks = (p.ntasks + 7) / 8;
-  int64_t cap = (int64_t)num_sms() * 8;
+  const int64_t cap = (int64_t)num_sms() * CPFIT_MTTKRP_MINB;
   const unsigned grid = (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
   const bool full = p.rank == LPE * VEC * KV;
   constexpr bool HOT = (sizeof(T) == 8 && VEC == 2) || (sizeof(T) == 4 && VEC == 4);
@@ -397,10 +412,10 @@ static int launch_mttkrp_np(const MttkrpParams<T> &p, cudaStream_t s) {
   return CPFIT_OK;
 }
 
-// Tiling policies (tools/tiling_sweep.py, profiles/r1_tiling_sweep.md):
+// Tiling policies (tools/tiling_sweep.py, profiles/r1_tuning.md):
 //  TTTP   -- 8 lanes per nonzero (LPE = 8, fewer when the row is narrower),
 //            KV = ceil(nv / 8) vectors per lane.
-//  MTTKRP -- fp64: 2 vectors per lane; fp32: 1 vector per lane.
+//  MTTKRP -- CPFIT_MTTKRP_KVT64 vectors per lane for fp64, 1 for fp32.
 // (lpe, kv) pairs outside the instantiated set fall back to LPE = 32.
 template <typename F>
 static int tttp_tiling_dispatch(int nv, F &&f) {
@@ -460,7 +475,7 @@ int dispatch_tttp(const TttpParams<T> &p, int vec, cudaStream_t s) {
 template <typename T>
 int dispatch_mttkrp(const MttkrpParams<T> &p, int vec, cudaStream_t s) {
   const int nv = (p.rank + vec - 1) / vec;
-  constexpr int KVT = sizeof(T) == 8 ? 2 : 1;
+  constexpr int KVT = sizeof(T) == 8 ? CPFIT_MTTKRP_KVT64 : 1;
   if constexpr (sizeof(T) == 8) {
     if (vec == 2)
       return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 2, L, K>(p, s); });
