@@ -214,6 +214,94 @@ def cpu_baseline_sample(seconds=12.0):
                       "oracle/cpfit_oracle.c on all host threads"}
 
 
+CPU_ALS_SURVEY_S = 125.0   # reference ALS sweep, cfg 3 full, 8 vCPU (SURVEY.md 6 / BASELINE.md 2)
+CPU_CCD_SURVEY_S = 562.0   # reference CCD++ sweep, same host
+
+
+def als_section(world, rank, dev, sweeps=2):
+    """BASELINE cfg 3 (480,189 x 17,770 x 2,182, 100,480,507 Zipf nnz, R=32,
+    lambda=1e-5): device-generated seeded instance; ALS sweep time at N GPUs
+    (row-sharded with an NCCL all-gather per mode when N > 1; strong scaling),
+    plus one CCD++ sweep on a single GPU."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1910_02371_b200 as cp
+    from paper_1910_02371_b200 import synth
+    from paper_1910_02371_b200.optim import _als_ls_device, _ccd_ls_device
+    R3, REG = 32, 1e-5
+    t0 = time.perf_counter()
+    shape, keys, vals = synth.cfg3_device()
+    gen_s = time.perf_counter() - t0
+    g = cp.RngState(0).child(0).generator()
+    init = [torch.from_numpy(g.random((d, R3)) / np.sqrt(R3)).to(dev) for d in shape]
+    stream = torch.cuda.current_stream()
+    out = {"workload": "BASELINE cfg 3 shape/nnz: 480189x17770x2182, 100480507 nnz, modes 0/1 "
+                       "Zipf(1), mode 2 uniform, values 1..5; R=32, lambda=1e-5 (direct solve)",
+           "generation_s": gen_s, "n_gpus": world}
+    if world == 1:
+        t = cp.SparseTensor.from_device(shape, keys, vals)
+        del keys
+        F = [f.clone() for f in init]
+        t1 = time.perf_counter()
+        _als_ls_device(t, F, REG)  # warm-up sweep: builds the mode layouts
+        torch.cuda.synchronize()
+        out["first_sweep_incl_layout_s"] = time.perf_counter() - t1
+        times = []
+        for _ in range(sweeps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _als_ls_device(t, F, REG)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        out["als_sweep_ms"] = float(np.mean(times))
+        from paper_1910_02371_b200.losses import ls_data_term
+        out["rmse_after"] = float(np.sqrt(ls_data_term(t, F) / t.nnz))
+        F = [f.clone() for f in init]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _ccd_ls_device(t, F, REG)
+        b.record(stream)
+        torch.cuda.synchronize()
+        out["ccd_sweep_ms"] = a.elapsed_time(b)
+        out["ccd_sweep_cpu_reference_s"] = CPU_CCD_SURVEY_S
+    else:
+        from paper_1910_02371_b200 import dist as D
+        coords = []
+        rem = keys.clone()
+        for d in reversed(shape):
+            coords.append(rem % d)
+            rem = rem // d
+        coords = coords[::-1]
+        del rem
+        als = D.ShardedALS(coords, vals, shape, REG, D.DeviceBackend())
+        del coords, keys
+        F = [f.clone() for f in init]
+        als.sweep(F)
+        torch.cuda.synchronize()
+        dist.barrier()
+        times = []
+        for _ in range(sweeps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            als.sweep(F)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            times.append(float(ms.item()))
+        out["als_sweep_ms"] = float(np.mean(times))
+        out["parallelism"] = f"row-sharded x{world}, NCCL all-gather of factor rows per mode"
+    out["als_sweep_cpu_reference_s"] = CPU_ALS_SURVEY_S
+    out["als_speedup_vs_cpu_reference"] = CPU_ALS_SURVEY_S * 1e3 / out["als_sweep_ms"]
+    out["cpu_reference_note"] = ("reference cpfit (numba + OpenBLAS, 8 vCPU Xeon) measured in "
+                                 "the survey container; see BASELINE.md 2")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -222,6 +310,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-als", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -409,6 +498,15 @@ def main():
                "path": "paper_1910_02371_b200.tttp/mttkrp with numpy (pinned) values and "
                        "factors; values re-uploaded and re-permuted every step"}
 
+    als = None
+    if not args.no_als:
+        del t, tout, mouts, svals, vals
+        torch.cuda.empty_cache()
+        try:
+            als = als_section(world, rank, dev)
+        except Exception as exc:  # reported, never fatal to the headline line
+            als = {"error": repr(exc)}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
@@ -419,6 +517,7 @@ def main():
             "roofline": roofline, "kernels": kernels, "gather_ceiling": probe,
             "compulsory_bytes_per_pass": compulsory,
             "clocks": clk, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
+            "als": als,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample()

@@ -286,6 +286,24 @@ class SparseTensor:
         t._keys_fn = keys_fn
         return t
 
+    @classmethod
+    def from_device(cls, shape, keys, values) -> "SparseTensor":
+        """Tensor whose sorted keys (int64/uint64 CUDA tensor) and values live
+        on the device already: the pattern is built straight from them and
+        host copies materialise only if ``keys`` / ``values`` are read."""
+        shape = check_shape(shape)
+        if keys.numel() != values.numel():
+            raise ValueError("keys and values must be 1-D of equal length")
+        shared = _Shared(pattern=DevicePattern.from_keys(shape, keys))
+        host = {}
+
+        def keys_fn():
+            if "k" not in host:
+                host["k"] = keys.cpu().numpy().view(np.uint64)
+            return host["k"]
+        return cls._device_born(shape, keys.numel(), shared, values.contiguous(),
+                                keys_fn=keys_fn)
+
     @property
     def keys(self) -> np.ndarray:
         if self._keys is None:

@@ -1,0 +1,173 @@
+"""Multi-GPU sharding of the completion sweeps (one process per GPU, NCCL).
+
+SURVEY.md 8(e): ALS shards *rows*.  For every mode n the rows of mode n are
+cut into P contiguous blocks balanced by the nonzero prefix sum (Zipf rows
+make equal row counts useless); rank p keeps a *mode shard*: the nonzeros
+whose mode-n index lies in its block, with that coordinate rebased to the
+block (shape[n] = block rows) and every other coordinate global.  Right-hand
+side (MTTKRP), Gram and solve are all row-local, so one mode update is:
+local MTTKRP + fused Gram/solve on the shard, then one all-gather of the
+updated I_n x R rows (blocks padded to the largest block; NCCL over
+NVLink/NVSwitch).  No other exchange: factors are replicated.
+
+SGD shards *nonzeros* (contiguous key ranges); the device Philox sampler uses
+the global entry index as its counter, so the union of the shard samples is
+the single-device sample bit for bit, and the per-mode gradients are summed
+with one all-reduce.
+
+The partition / shard / assembly logic is backend-neutral: ``LocalBackend``
+objects supply the row-local compute.  ``DeviceBackend`` runs the CUDA
+kernels; tests (tests/test_dist.py, gloo, world size 2 on CPU) plug in the CPU
+oracle to check the distributed algebra without a GPU.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def row_partition(row_counts, parts: int):
+    """Contiguous row blocks [lo, hi) balanced by the nnz prefix sum."""
+    counts = np.asarray(row_counts, dtype=np.int64)
+    prefix = np.concatenate([[0], np.cumsum(counts)])
+    total = int(prefix[-1])
+    bounds = [0]
+    for p in range(1, parts):
+        target = total * p / parts
+        r = int(np.searchsorted(prefix, target, side="left"))
+        r = max(bounds[-1], min(r, counts.size))
+        bounds.append(r)
+    bounds.append(counts.size)
+    return [(bounds[i], bounds[i + 1]) for i in range(parts)]
+
+
+def nnz_partition(nnz: int, parts: int, align: int = 4):
+    """Contiguous nonzero ranges (aligned so Philox blocks of 4 draws are not
+    split across ranks; any split would still be bit-exact)."""
+    out = []
+    for p in range(parts):
+        lo = (nnz * p // parts) // align * align
+        hi = nnz if p == parts - 1 else (nnz * (p + 1) // parts) // align * align
+        out.append((lo, hi))
+    return out
+
+
+def shard_keys(coords, shape, mode: int, lo: int, hi: int, xp=np):
+    """Select entries with lo <= i_mode < hi and re-linearize with the mode
+    rebased; returns (shard shape, keys, selection mask).  ``xp`` is numpy or
+    torch (coords as int64 arrays of the backend)."""
+    sel = (coords[mode] >= lo) & (coords[mode] < hi)
+    sshape = list(shape)
+    sshape[mode] = max(hi - lo, 1)
+    key = None
+    for n, d in enumerate(sshape):
+        c = coords[n][sel]
+        if n == mode:
+            c = c - lo
+        key = c if key is None else key * d + c
+    return tuple(sshape), key, sel
+
+
+def pad_rows(x, rows: int, xp=np):
+    if x.shape[0] == rows:
+        return x
+    if xp is np:
+        out = np.zeros((rows,) + tuple(x.shape[1:]), dtype=x.dtype)
+    else:
+        out = xp.zeros((rows,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    out[: x.shape[0]] = x
+    return out
+
+
+class ShardedALS:
+    """Row-sharded ALS sweeps over a process group.
+
+    backend: object with
+      make_shard(shape, keys, values) -> handle
+      als_mode(handle, factors, mode, reg) -> updated rows of the block
+      to_comm(x) / from_comm(x) -> tensors for torch.distributed
+      xp -> numpy or torch (for shard_keys / padding)
+    """
+
+    def __init__(self, coords, values, shape, reg, backend, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.shape = tuple(shape)
+        self.reg = float(reg)
+        self.backend = backend
+        xp = backend.xp
+        self.blocks = []
+        self.shards = []
+        for mode, d in enumerate(self.shape):
+            if xp is np:
+                counts = np.bincount(coords[mode], minlength=d)
+            else:
+                counts = xp.bincount(coords[mode], minlength=d).cpu().numpy()
+            blocks = row_partition(counts, self.world)
+            lo, hi = blocks[self.rank]
+            sshape, keys, sel = shard_keys(coords, self.shape, mode, lo, hi, xp)
+            self.blocks.append(blocks)
+            self.shards.append(backend.make_shard(sshape, keys, values[sel]))
+
+    def mode_update(self, factors, mode: int):
+        blocks = self.blocks[mode]
+        lo, hi = blocks[self.rank]
+        rows = self.backend.als_mode(self.shards[mode], factors, mode, self.reg, lo, hi)
+        maxr = max(b - a for a, b in blocks)
+        send = self.backend.to_comm(pad_rows(rows, maxr, self.backend.xp))
+        recv = self.backend.empty_comm((self.world * maxr,) + tuple(send.shape[1:]), send)
+        self.dist.all_gather_into_tensor(recv, send, group=self.group)
+        parts = [recv[p * maxr: p * maxr + (b - a)] for p, (a, b) in enumerate(blocks)]
+        full = self.backend.cat(parts)
+        factors[mode] = self.backend.from_comm(full)
+
+    def sweep(self, factors):
+        for mode in range(len(self.shape)):
+            self.mode_update(factors, mode)
+        return factors
+
+
+class DeviceBackend:
+    """CUDA kernels + NCCL (factors are CUDA tensors)."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+        self.xp = torch
+
+    def make_shard(self, shape, keys, values):
+        from .core import SparseTensor
+        return SparseTensor.from_device(shape, keys.contiguous(), values.contiguous())
+
+    def als_mode(self, shard, factors, mode, reg, lo, hi):
+        """Rows lo..hi of the updated factor: MTTKRP + Gram + solve on the shard,
+        with the shard's own (rebased) mode factor slot unused."""
+        from .optim import _als_mode_device
+        return _als_mode_device(shard, factors, mode, reg, row_offset=lo)
+
+    def to_comm(self, x):
+        return x.contiguous()
+
+    def from_comm(self, x):
+        return x.contiguous()
+
+    def empty_comm(self, shape, like):
+        return self.torch.empty(shape, dtype=like.dtype, device=like.device)
+
+    def cat(self, parts):
+        return self.torch.cat(parts, 0)
+
+
+def als_strong_scaling_rows(blocks):
+    """Largest block share (the load imbalance bound of a sharded sweep)."""
+    sizes = [b - a for a, b in blocks]
+    return max(sizes) / max(1, sum(sizes)) * len(sizes)
+
+
+__all__ = ["row_partition", "nnz_partition", "shard_keys", "ShardedALS", "DeviceBackend",
+           "pad_rows", "als_strong_scaling_rows", "math"]

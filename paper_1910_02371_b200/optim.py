@@ -208,42 +208,62 @@ def _stream():
 # ---------------------------------------------------------------------------
 # alternating minimization
 
-def _als_ls_device(t: SparseTensor, F, reg: float, keep_gram: bool = True):
-    """One least-squares ALS sweep on device factors F (list of CUDA tensors,
-    updated in place).  Returns per-mode (gram, rhs)."""
+def _als_mode_device(t: SparseTensor, F, mode: int, reg: float, keep_gram: bool = False,
+                     row_offset: int = 0):
+    """One least-squares ALS mode update on the device: rhs = MTTKRP of the
+    data, then the fused Gram assembly (unit weights: the observation mask is
+    never materialised) + batched SPD solve.  Returns x (or (x, gram, rhs))
+    with t.shape[mode] rows; F[mode] is not read (t's mode may be a rebased
+    row block of a larger factor -- dist.ShardedALS)."""
     torch = _torch()
-    dtype = F[0].dtype
+    dtype = F[0].dtype if F[0] is not None else F[1].dtype
+    dev = next(f for f in F if f is not None).device
     code = _dtype_code(dtype)
-    rank = F[0].shape[1]
+    rank = next(f for f in F if f is not None).shape[1]
     L = _lib.load()
     pat = t.device_pattern()
+    ptrs = _ptrs([None if n == mode else f for n, f in enumerate(F)])
+    rhs = torch.empty((t.shape[mode], rank), dtype=dtype, device=dev)
+    if t.nnz:
+        vals = t.sorted_values(mode, dtype)
+        _lib.check(L.cpfit_mttkrp(pat.handle, mode, code, rank,
+                                  ctypes.c_void_p(vals.data_ptr()), 1, ptrs,
+                                  ctypes.c_void_p(rhs.data_ptr()), _stream()), "mttkrp")
+    else:
+        rhs.zero_()
+    x = torch.empty_like(rhs)
+    gram = torch.empty((t.shape[mode], rank, rank), dtype=dtype, device=dev) \
+        if keep_gram else None
+    bad = ctypes.c_int64(-1)
+    st = L.cpfit_solve_factor(pat.handle, mode, code, rank, None, 1, ptrs,
+                              ctypes.c_void_p(rhs.data_ptr()), float(reg),
+                              ctypes.c_void_p(x.data_ptr()),
+                              ctypes.c_void_p(0 if gram is None else gram.data_ptr()),
+                              ctypes.byref(bad), _stream())
+    if st == _lib.EEMPTYROW:
+        raise NumericalError(
+            f"alternating solve failed: mode {mode} row {bad.value + row_offset}: no incident "
+            "entries and reg=0 but right-hand side is nonzero")
+    if st == _lib.ESINGULAR:
+        raise NumericalError(f"alternating solve failed: mode {mode} row "
+                             f"{bad.value + row_offset}: singular normal equations "
+                             f"(reg={float(reg)})")
+    _lib.check(st, "solve_factor")
+    if keep_gram:
+        return x, gram, rhs
+    return x
+
+
+def _als_ls_device(t: SparseTensor, F, reg: float, keep_gram: bool = True):
+    """One least-squares ALS sweep on device factors F (list of CUDA tensors,
+    updated in place, modes in order, optim.py:194-206).  Returns per-mode
+    (gram, rhs)."""
     grams, rhss = [], []
     for mode in range(t.order):
-        rhs = torch.empty((t.shape[mode], rank), dtype=dtype, device=F[0].device)
-        if t.nnz:
-            vals = t.sorted_values(mode, dtype)
-            _lib.check(L.cpfit_mttkrp(pat.handle, mode, code, rank,
-                                      ctypes.c_void_p(vals.data_ptr()), 1, _ptrs(F),
-                                      ctypes.c_void_p(rhs.data_ptr()), _stream()), "mttkrp")
+        if keep_gram:
+            x, gram, rhs = _als_mode_device(t, F, mode, reg, keep_gram=True)
         else:
-            rhs.zero_()
-        x = torch.empty_like(rhs)
-        gram = torch.empty((t.shape[mode], rank, rank), dtype=dtype, device=F[0].device) \
-            if keep_gram else None
-        bad = ctypes.c_int64(-1)
-        st = L.cpfit_solve_factor(pat.handle, mode, code, rank, None, 1, _ptrs(F),
-                                  ctypes.c_void_p(rhs.data_ptr()), float(reg),
-                                  ctypes.c_void_p(x.data_ptr()),
-                                  ctypes.c_void_p(0 if gram is None else gram.data_ptr()),
-                                  ctypes.byref(bad), _stream())
-        if st == _lib.EEMPTYROW:
-            raise NumericalError(
-                f"alternating solve failed: mode {mode} row {bad.value}: no incident entries "
-                "and reg=0 but right-hand side is nonzero")
-        if st == _lib.ESINGULAR:
-            raise NumericalError(f"alternating solve failed: mode {mode} row {bad.value}: "
-                                 f"singular normal equations (reg={float(reg)})")
-        _lib.check(st, "solve_factor")
+            x, gram, rhs = _als_mode_device(t, F, mode, reg), None, None
         F[mode] = x
         grams.append(gram)
         rhss.append(rhs)

@@ -138,3 +138,39 @@ def cfg5(seed: int = CFG5_SEED, nnz: int = 1_000_000_000,
     values = (_model_values(truth, coords) + rng.normal(0.0, 0.1, keys.size))
     factors = [(rng.standard_normal((d, rank)) * np.sqrt(1.0 / rank)) for d in shape]
     return shape, keys, values.astype(np.float32), [f.astype(np.float32) for f in factors]
+
+
+def cfg3_device(seed: int = CFG3_SEED, nnz: int = 100_480_507,
+                shape=(480_189, 17_770, 2_182), device="cuda"):
+    """cfg 3 synthesised on the GPU (torch RNG, same laws as ``cfg3``):
+    returns (shape, sorted int64 keys on device, f64 values on device).
+    Seconds instead of minutes at full size; deterministic for a given seed
+    and GPU type.  Used by the ALS / CCD++ benchmarks."""
+    import torch
+    shape = tuple(int(d) for d in shape)
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+
+    def zipf(dim, size):
+        w = 1.0 / torch.arange(1, dim + 1, dtype=torch.float64, device=device)
+        cdf = torch.cumsum(w, 0)
+        cdf /= cdf[-1].clone()
+        u = torch.rand(size, generator=g, dtype=torch.float64, device=device)
+        return torch.clamp(torch.searchsorted(cdf, u, right=True), max=dim - 1)
+
+    keys = torch.empty(0, dtype=torch.int64, device=device)
+    draws = int(nnz * 1.05)
+    while keys.numel() < nnz:
+        i0 = zipf(shape[0], draws)
+        i1 = zipf(shape[1], draws)
+        i2 = torch.randint(0, shape[2], (draws,), generator=g, device=device)
+        k = (i0 * shape[1] + i1) * shape[2] + i2
+        del i0, i1, i2
+        keys = torch.unique(torch.cat([keys, k]))
+        del k
+        draws = max(int((nnz - keys.numel()) * 1.5), 1024)
+    if keys.numel() > nnz:
+        pick = torch.randperm(keys.numel(), generator=g, device=device)[:nnz]
+        keys = keys[torch.sort(pick).values]
+    values = torch.randint(1, 6, (nnz,), generator=g, device=device).to(torch.float64)
+    return shape, keys, values

@@ -1,0 +1,160 @@
+"""Multi-process (gloo, world size 2, CPU) tests of the sharding logic in
+paper_1910_02371_b200.dist, with the CPU oracle as the row-local compute:
+the row-sharded ALS sweep with an all-gather of factor rows must reproduce
+the single-process sweep bit for bit; the nonzero-sharded SGD sample must be
+the single-process sample bit for bit and the all-reduced gradients must
+match within 1e-12."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_1910_02371_b200 import dist as D
+from paper_1910_02371_b200 import synth
+
+
+class OracleBackend:
+    xp = np
+
+    def make_shard(self, shape, keys, values):
+        return O.OTensor(tuple(int(d) for d in shape), np.asarray(keys, dtype=np.uint64),
+                         np.asarray(values, dtype=np.float64))
+
+    def als_mode(self, shard, factors, mode, reg, lo, hi):
+        fs = [None if n == mode else f for n, f in enumerate(factors)]
+        rhs = O.mttkrp(shard, fs, mode)
+        mask = shard.with_values(np.ones(shard.nnz))
+        return O.solve_factor(mask, fs, rhs, mode, reg=reg)
+
+    def to_comm(self, x):
+        return torch.from_numpy(np.ascontiguousarray(x))
+
+    def from_comm(self, x):
+        return x.numpy().copy()
+
+    def empty_comm(self, shape, like):
+        return torch.empty(shape, dtype=like.dtype)
+
+    def cat(self, parts):
+        return torch.cat(parts, 0)
+
+
+def _instance(nnz=20_000):
+    rng = np.random.default_rng(42)
+    shape = (300, 120, 50)
+    i0 = synth.zipf_indices(rng, shape[0], nnz)
+    i1 = synth.zipf_indices(rng, shape[1], nnz)
+    i2 = rng.integers(0, shape[2], nnz)
+    keys = np.unique((i0 * shape[1] + i1) * shape[2] + i2).astype(np.uint64)
+    values = rng.integers(1, 6, keys.size).astype(np.float64)
+    factors = [rng.random((d, 8)) / np.sqrt(8) for d in shape]
+    return shape, keys, values, factors
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shape, keys, values, factors = _instance()
+        coords = O.delinearize(keys, shape)
+        als = D.ShardedALS(coords, values, shape, 1e-5, OracleBackend())
+        fs = [f.copy() for f in factors]
+        for _ in range(2):
+            als.sweep(fs)
+        np.savez(os.path.join(outdir, f"als{rank}.npz"), *fs,
+                 blocks=np.array(als.blocks, dtype=np.int64))
+        # SGD: nonzero shards, global Philox counter, all-reduced gradients
+        lo, hi = D.nnz_partition(keys.size, world)[rank]
+        seed, path, rate = 7, (1, 1), 0.3
+        draws = O.uniform(seed, path, hi - lo, start=lo)
+        kept_local = np.flatnonzero(draws < rate) + lo
+        fs = [f.copy() for f in factors]
+        ot = O.OTensor(shape, keys[kept_local], values[kept_local])
+        if ot.nnz:
+            model = O.tttp(ot.with_values(np.ones(ot.nnz)), fs)
+            phi1 = ot.with_values(2.0 * (model - ot.values))
+            grads = [O.mttkrp(phi1, fs, m) for m in range(3)]
+        else:
+            grads = [np.zeros_like(f) for f in fs]
+        summed = []
+        for g in grads:
+            tg = torch.from_numpy(g)
+            dist.all_reduce(tg)
+            summed.append(tg.numpy())
+        np.savez(os.path.join(outdir, f"sgd{rank}.npz"), kept=kept_local, *summed)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def dist_run(tmp_path_factory):
+    out = tmp_path_factory.mktemp("dist")
+    mp.spawn(_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
+    return out
+
+
+def test_row_partition_balances_skewed_rows():
+    counts = np.array([1000, 1, 1, 1, 500, 500, 3, 3])
+    blocks = D.row_partition(counts, 2)
+    assert blocks[0][0] == 0 and blocks[-1][1] == counts.size
+    assert blocks[0][1] == blocks[1][0]
+    assert D.row_partition(np.ones(10), 3) == [(0, 3), (3, 7), (7, 10)] or \
+        sum(b - a for a, b in D.row_partition(np.ones(10), 3)) == 10
+    parts = D.nnz_partition(1001, 4)
+    assert parts[0][0] == 0 and parts[-1][1] == 1001
+    assert all(a % 4 == 0 for a, _ in parts)
+
+
+def test_shard_keys_rebase_and_order():
+    shape, keys, values, _ = _instance(2000)
+    coords = O.delinearize(keys, shape)
+    sshape, skeys, sel = D.shard_keys(coords, shape, 1, 10, 40)
+    assert sshape == (shape[0], 30, shape[2])
+    assert np.all(np.diff(skeys) > 0)  # canonical order preserved
+    sc = O.delinearize(skeys.astype(np.uint64), sshape)
+    assert np.array_equal(sc[1] + 10, coords[1][sel])
+    assert np.array_equal(sc[0], coords[0][sel])
+
+
+def test_sharded_als_bitwise_equals_single_process(dist_run):
+    shape, keys, values, factors = _instance()
+    ot = O.OTensor(shape, keys, values)
+    fs = [f.copy() for f in factors]
+    for _ in range(2):
+        O.als_sweep(ot, fs, 1e-5)
+    for rank in range(2):
+        z = np.load(os.path.join(dist_run, f"als{rank}.npz"))
+        for n in range(3):
+            assert np.array_equal(z[f"arr_{n}"], fs[n]), (rank, n)
+
+
+def test_sharded_sgd_sample_and_gradients(dist_run):
+    shape, keys, values, factors = _instance()
+    ot = O.OTensor(shape, keys, values)
+    kept = O.sample_positions(ot, 0.3, 7, (1, 1))
+    z0 = np.load(os.path.join(dist_run, "sgd0.npz"))
+    z1 = np.load(os.path.join(dist_run, "sgd1.npz"))
+    assert np.array_equal(np.concatenate([z0["kept"], z1["kept"]]), kept)
+    s = O.sample(ot, 0.3, 7, (1, 1))
+    model = O.tttp(s.with_values(np.ones(s.nnz)), factors)
+    phi1 = s.with_values(2.0 * (model - s.values))
+    for m in range(3):
+        ref = O.mttkrp(phi1, factors, m)
+        got = z0[f"arr_{m}"]
+        assert np.array_equal(got, z1[f"arr_{m}"])
+        assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
