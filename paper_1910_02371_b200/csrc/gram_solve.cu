@@ -4,19 +4,24 @@
 // Gram: G_i = sum_{e in row i} (sqrt(w_e) h_e)(sqrt(w_e) h_e)^T with
 // h_e = prod_{k != mode} A_k[i_k(e), :] -- exactly the reference's staged
 // rank-k update (kernels.py:195-205).  One warp per mode-sorted task stages
-// 32 Hadamard rows at a time in shared memory and accumulates G with FP64
-// tensor-core MMAs (mma.sync m8n8k4 f64 -> DMMA; tcgen05 has no f64 kind),
-// computing only the upper-triangular 8x8 tiles (G is symmetric) and
-// mirroring on store.  Long rows are split into tasks whose partial Grams
-// are summed in task order (deterministic; no floating-point atomics).
+// 32 Hadamard rows at a time in shared memory (lane groups gather the factor
+// rows with vector loads, several nonzeros per warp instruction, loads for
+// U slots issued before use) and accumulates G with FP64 tensor-core MMAs
+// (mma.sync m8n8k4 f64 -> DMMA; tcgen05 has no f64 kind), computing only the
+// upper-triangular 8x8 tiles (G is symmetric) and mirroring on store.  Long
+// rows are split into tasks whose partial Grams are summed in task order
+// (deterministic; no floating-point atomics).
 //
-// Solve: one warp per row factors (G_i + reg I) with a shared-memory
-// Cholesky; a row whose Cholesky hits a non-positive pivot is re-solved with
-// partial-pivoting LU, which reports "singular" exactly when LAPACK gesv
-// (np.linalg.solve, kernels.py:259) would: on an exact zero pivot.  Empty
-// rows follow kernels.py:245-257 (x = rhs/reg, or identity when reg == 0 with
-// an error for a nonzero rhs).  The first offending row is found with an
-// integer atomicMin (order independent).
+// Solve: for R <= 32 one warp per row keeps G + reg I in registers (lane j
+// owns column j) and runs a right-looking Cholesky whose column broadcasts
+// also drive the forward substitution, then back-substitutes with one
+// shuffle per step -- no shared memory, no barriers.  Rows whose Cholesky
+// meets a non-positive pivot (and every row when R > 32) go through a
+// shared-memory kernel with a partial-pivoting LU fallback that reports
+// "singular" exactly when LAPACK gesv (np.linalg.solve, kernels.py:259)
+// would: on an exact zero pivot.  Empty rows follow kernels.py:245-257
+// (x = rhs/reg, or identity when reg == 0 with an error for a nonzero rhs).
+// The first offending row is found with an integer atomicMin.
 #include <cfloat>
 
 #include "common.cuh"
@@ -54,16 +59,30 @@ constexpr int gram_ld() {
   return RT * 8 + 8;  // +8 doubles: rows 64 B apart in bank space
 }
 
-template <typename T, int RT>
+constexpr int pow2_at_least(int x) {
+  int p = 1;
+  while (p < x && p < 32) p *= 2;
+  return p;
+}
+
+template <typename T, int RT, int VEC, int NPT>
 __global__ void __launch_bounds__(GRAM_WARPS * 32)
 gram_kernel(const GramParams<T> p) {
   constexpr int RP = RT * 8;
   constexpr int LD = gram_ld<RT>();
-  constexpr int NT = RT * (RT + 1) / 2;  // upper-triangular tiles
+  constexpr int NT = RT * (RT + 1) / 2;           // upper-triangular tiles
+  constexpr int NV = RP / VEC;                    // vectors per padded row
+  constexpr int LPE = pow2_at_least(NV);          // lanes per staged entry
+  constexpr int KV = (NV + LPE - 1) / LPE;
+  constexpr int G = 32 / LPE;                     // entries per warp instruction
+  constexpr int U = LPE < 4 ? LPE : 4;            // sub-iterations batched
+  constexpr int NPM = NPT > 0 ? NPT : CPFIT_MAXN;
   extern __shared__ double gsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int g = lane / LPE, q = lane % LPE;
   double *H = gsm + (size_t)wib * GRAM_CHUNK * LD;
   const int rank = p.rank;
+  const int np = NPT > 0 ? NPT : p.np;
   const int64_t warp = (int64_t)blockIdx.x * GRAM_WARPS + wib;
   const int64_t nwarps = (int64_t)gridDim.x * GRAM_WARPS;
   const int gq = lane >> 2, tq = lane & 3;
@@ -78,37 +97,65 @@ gram_kernel(const GramParams<T> p) {
       const int cnt = (int)(b1 - base < GRAM_CHUNK ? b1 - base : GRAM_CHUNK);
       // coalesced index / weight loads, one entry per lane
       const int64_t e = base + lane;
-      int32_t my_idx[CPFIT_MAXN];
+      int32_t my_idx[NPM];
 #pragma unroll
-      for (int n = 0; n < CPFIT_MAXN; ++n)
-        my_idx[n] = (n < p.np && lane < cnt) ? __ldg(p.idx[n] + e) : 0;
-      double my_sw = 1.0;
-      if (p.weights && lane < cnt) {
-        T w = p.wperm ? __ldg(p.weights + __ldg(p.wperm + e)) : __ldg(p.weights + e);
-        my_sw = sqrt((double)w);
+      for (int n = 0; n < NPM; ++n) my_idx[n] = (n < np && lane < cnt) ? __ldg(p.idx[n] + e) : 0;
+      double my_sw = 0.0;  // padded slots stage zero rows
+      if (lane < cnt) {
+        my_sw = 1.0;
+        if (p.weights) {
+          T w = p.wperm ? __ldg(p.weights + __ldg(p.wperm + e)) : __ldg(p.weights + e);
+          my_sw = sqrt((double)w);
+        }
       }
-      // stage sqrt(w) * h rows: the warp gathers one factor row per step
-#pragma unroll 4
-      for (int j = 0; j < GRAM_CHUNK; ++j) {
-        const double sw = __shfl_sync(0xffffffffu, my_sw, j);
-        int rows[CPFIT_MAXN];
+      // stage sqrt(w) * h rows: group g handles slot j = s*G + g
 #pragma unroll
-        for (int n = 0; n < CPFIT_MAXN; ++n)
-          if (n < p.np) rows[n] = __shfl_sync(0xffffffffu, my_idx[n], j);
+      for (int s0 = 0; s0 < LPE; s0 += U) {
+        T x[U][NPM][KV][VEC];
 #pragma unroll
-        for (int c0 = 0; c0 < RP; c0 += 32) {
-          const int c = c0 + lane;
-          double h = 0.0;
-          if (j < cnt && c < rank) {
+        for (int u = 0; u < U; ++u) {
+          const int j = (s0 + u) * G + g;
 #pragma unroll
-            for (int n = 0; n < CPFIT_MAXN; ++n) {
-              if (n >= p.np) break;
-              const double a = (double)__ldg(p.fac[n] + (int64_t)rows[n] * rank + c);
-              h = (n == 0) ? a : h * a;
+          for (int n = 0; n < NPM; ++n) {
+            if (n >= np) break;
+            const unsigned row = (unsigned)__shfl_sync(0xffffffffu, my_idx[n], j);
+            const T *frow = p.fac[n] + (size_t)row * (unsigned)rank;
+#pragma unroll
+            for (int k = 0; k < KV; ++k) {
+              const int col = (k * LPE + q) * VEC;
+              if (col < rank) {
+                load_vec<T, VEC>(frow + col, x[u][n][k]);
+              } else {
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) x[u][n][k][v] = T(0);
+              }
             }
-            h *= sw;
           }
-          if (c < RP) H[j * LD + c] = h;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = (s0 + u) * G + g;
+          const double sw = __shfl_sync(0xffffffffu, my_sw, j);
+#pragma unroll
+          for (int k = 0; k < KV; ++k) {
+            const int col = (k * LPE + q) * VEC;
+            double h[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              double prod = (double)x[u][0][k][v];
+#pragma unroll
+              for (int n = 1; n < NPM; ++n)
+                if (n < np) prod *= (double)x[u][n][k][v];
+              h[v] = prod * sw;
+            }
+            if (col < RP) {
+              if constexpr (VEC == 2) {
+                *reinterpret_cast<double2 *>(H + j * LD + col) = make_double2(h[0], h[1]);
+              } else {
+                H[j * LD + col] = h[0];
+              }
+            }
+          }
         }
       }
       __syncwarp();
@@ -121,8 +168,8 @@ gram_kernel(const GramParams<T> p) {
 #pragma unroll
         for (int i = 0; i < RT; ++i)
 #pragma unroll
-          for (int j = i; j < RT; ++j) {
-            dmma_8x8x4(acc[tile][0], acc[tile][1], f[i], f[j]);
+          for (int jt = i; jt < RT; ++jt) {
+            dmma_8x8x4(acc[tile][0], acc[tile][1], f[i], f[jt]);
             ++tile;
           }
       }
@@ -136,13 +183,13 @@ gram_kernel(const GramParams<T> p) {
 #pragma unroll
     for (int i = 0; i < RT; ++i)
 #pragma unroll
-      for (int j = i; j < RT; ++j) {
+      for (int jt = i; jt < RT; ++jt) {
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int r = 8 * i + gq, c = 8 * j + 2 * tq + v;
+          const int r = 8 * i + gq, c = 8 * jt + 2 * tq + v;
           if (r < rank && c < rank) {
             dst[(int64_t)r * rank + c] = (T)acc[tile][v];
-            if (i != j) dst[(int64_t)c * rank + r] = (T)acc[tile][v];
+            if (i != jt) dst[(int64_t)c * rank + r] = (T)acc[tile][v];
           }
         }
         ++tile;
@@ -155,8 +202,7 @@ __global__ void combine_gram_partials(const int32_t *__restrict__ split_row,
                                       const int32_t *__restrict__ split_slot, int64_t nsplit,
                                       int64_t rr, const T *__restrict__ partial,
                                       T *__restrict__ gram) {
-  const int64_t blk = blockIdx.x;
-  for (int64_t s = blk; s < nsplit; s += gridDim.x) {
+  for (int64_t s = blockIdx.x; s < nsplit; s += gridDim.x) {
     const int64_t row = split_row[s];
     const int64_t a = split_slot[s], b = split_slot[s + 1];
     for (int64_t c = threadIdx.x; c < rr; c += blockDim.x) {
@@ -177,22 +223,35 @@ __global__ void check_weights_kernel(const T *__restrict__ w, int64_t n, int *fl
   if (bad && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
-template <typename T, int RT>
-static int launch_gram_rt(const GramParams<T> &p, cudaStream_t s) {
+template <typename T, int RT, int VEC, int NPT>
+static int launch_gram_v(const GramParams<T> &p, cudaStream_t s) {
   constexpr int LD = gram_ld<RT>();
   const size_t smem = (size_t)GRAM_WARPS * GRAM_CHUNK * LD * sizeof(double);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(gram_kernel<T, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(gram_kernel<T, RT, VEC, NPT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   int64_t blocks = (p.ntasks + GRAM_WARPS - 1) / GRAM_WARPS;
   int64_t cap = (int64_t)num_sms() * 8;
   unsigned grid = (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
-  gram_kernel<T, RT><<<grid, GRAM_WARPS * 32, smem, s>>>(p);
+  gram_kernel<T, RT, VEC, NPT><<<grid, GRAM_WARPS * 32, smem, s>>>(p);
   CPFIT_LAUNCH_CHECK("gram_kernel");
   return CPFIT_OK;
+}
+
+template <typename T, int RT>
+static int launch_gram_rt(const GramParams<T> &p, cudaStream_t s) {
+  bool vec2 = (p.rank % 2 == 0);
+  for (int n = 0; n < p.np; ++n)
+    if ((uintptr_t)p.fac[n] % (2 * sizeof(T))) vec2 = false;
+  if (vec2) {
+    if (p.np == 2) return launch_gram_v<T, RT, 2, 2>(p, s);
+    return launch_gram_v<T, RT, 2, 0>(p, s);
+  }
+  if (p.np == 2) return launch_gram_v<T, RT, 1, 2>(p, s);
+  return launch_gram_v<T, RT, 1, 0>(p, s);
 }
 
 template <typename T>
@@ -287,7 +346,111 @@ struct SolveParams {
   double reg;
   T *x;
   unsigned long long *bad;  // [0] first empty row with nonzero rhs, [1] first singular row
+  const int32_t *rows;      // smem kernel: explicit row list (null: rows 0..dim-1)
+  int64_t nrows;
+  int32_t *retry;           // register kernel: rows whose Cholesky failed
+  unsigned long long *nretry;
 };
+
+// Empty row (kernels.py:245-257): reg*I system (x = rhs/reg) or identity when
+// reg == 0 (error for a nonzero rhs).
+template <typename T>
+__device__ __forceinline__ void solve_empty_row(const SolveParams<T> &p, int64_t row) {
+  const int lane = threadIdx.x & 31;
+  const int R = p.rank;
+  bool nz = false;
+  for (int i = lane; i < R; i += 32) {
+    const double b = (double)p.rhs[row * R + i];
+    if (p.reg == 0.0) {
+      nz |= (b != 0.0);
+      p.x[row * R + i] = (T)b;
+    } else {
+      p.x[row * R + i] = (T)(b / p.reg);
+    }
+  }
+  if (__any_sync(0xffffffffu, nz) && lane == 0) atomicMin(&p.bad[0], (unsigned long long)row);
+}
+
+// Register-resident warp Cholesky solve for R <= RMAX <= 32.  Lane j holds
+// column j of (G + reg I) in a[] (G is stored symmetric, so column j = row j,
+// a contiguous load); b[] (right-hand side, then y, then x) is replicated in
+// every lane.  Step k broadcasts column k of L (one shuffle per element), which
+// every lane also uses for the forward substitution; lanes right of k apply
+// the trailing update to their own column.  Back substitution: lane k owns
+// L[:, k], so x_k needs one dot product on lane k and one broadcast.
+template <typename T, int RMAX>
+__device__ __forceinline__ bool chol_solve_row(const T *__restrict__ Gr, const T *__restrict__ rh,
+                                               int R, double reg, T *__restrict__ xo) {
+  const int lane = threadIdx.x & 31;
+  double a[RMAX], b[RMAX];
+#pragma unroll
+  for (int i = 0; i < RMAX; ++i) {
+    a[i] = (i < R && lane < R) ? (double)__ldg(Gr + lane * R + i) : 0.0;
+    b[i] = i < R ? (double)__ldg(rh + i) : 0.0;
+    if (i == lane) a[i] += reg;
+  }
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < RMAX; ++k) {
+    if (k < R) {
+      const double d = __shfl_sync(0xffffffffu, a[k], k);
+      if (!(d > 0.0) || !(d < DBL_MAX)) ok = false;
+      const double lkk = sqrt(d);
+      const double inv = 1.0 / lkk;
+      const double yk = b[k] * inv;
+      double ljk = 0.0;
+#pragma unroll
+      for (int i = k + 1; i < RMAX; ++i) {
+        if (i < R) {
+          const double ci = __shfl_sync(0xffffffffu, a[i], k) * inv;  // L[i][k]
+          if (i == lane) ljk = ci;
+          a[i] = lane == k ? ci : (lane > k ? fma(-ci, ljk, a[i]) : a[i]);
+          b[i] = fma(-ci, yk, b[i]);  // forward substitution, replicated
+        }
+      }
+      if (lane == k) a[k] = lkk;
+      b[k] = yk;
+    }
+  }
+  // back substitution L^T x = y (harmless garbage when !ok: not stored)
+#pragma unroll
+  for (int kk = 0; kk < RMAX; ++kk) {
+    const int k = RMAX - 1 - kk;
+    if (k < R) {
+      double sdot = 0.0;
+#pragma unroll
+      for (int i = k + 1; i < RMAX; ++i)
+        if (i < R) sdot = fma(a[i], b[i], sdot);
+      b[k] = __shfl_sync(0xffffffffu, (b[k] - sdot) / a[k], k);
+    }
+  }
+  double mine = 0.0;
+#pragma unroll
+  for (int i = 0; i < RMAX; ++i)
+    if (i == lane) mine = b[i];
+  if (!__all_sync(0xffffffffu, ok)) return false;
+  if (lane < R) xo[lane] = (T)mine;
+  return true;
+}
+
+// One warp per row and no grid-stride loop: inside a loop ptxas keeps the
+// fully unrolled register arrays on the stack.
+template <typename T, int RMAX>
+__global__ void __launch_bounds__(128) solve_reg_kernel(const SolveParams<T> p) {
+  const int lane = threadIdx.x & 31;
+  const int R = p.rank;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= p.dim) return;
+  if (p.offsets[row + 1] == p.offsets[row]) {
+    solve_empty_row(p, row);
+  } else if (!chol_solve_row<T, RMAX>(p.gram + row * (int64_t)R * R, p.rhs + row * (int64_t)R,
+                                      R, p.reg, p.x + row * (int64_t)R)) {
+    if (lane == 0) {
+      const unsigned long long slot = atomicAdd(p.nretry, 1ull);
+      p.retry[slot] = (int32_t)row;
+    }
+  }
+}
 
 // Partial-pivot LU of the R x R system in smem (row-major, leading dim ld),
 // right-hand side b[] distributed (element i held by lane i % 32, slot i / 32).
@@ -380,7 +543,9 @@ __global__ void solve_kernel(const SolveParams<T> p, int warps_per_block) {
   const int64_t warp = (int64_t)blockIdx.x * warps_per_block + wib;
   const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
 
-  for (int64_t row = warp; row < p.dim; row += nwarps) {
+  const int64_t nrows = p.rows ? p.nrows : p.dim;
+  for (int64_t it = warp; it < nrows; it += nwarps) {
+    const int64_t row = p.rows ? (int64_t)p.rows[it] : it;
     const bool empty = p.offsets[row + 1] == p.offsets[row];
     const T *rhs = p.rhs + row * R;
     T *xo = p.x + row * R;
@@ -487,28 +652,13 @@ __global__ void solve_kernel(const SolveParams<T> p, int warps_per_block) {
 }
 
 template <typename T>
-static int run_solve(cpfit_pattern *pt, int mode, int rank, const T *gram, const T *rhs,
-                     double reg, T *x, int64_t *bad_row, cudaStream_t s) {
-  CpfitModeLayout &L = pt->modes[mode];
-  const int64_t dim = pt->dims[mode];
-  Scratch<unsigned long long> bad(s);
-  CPFIT_TRY(bad.alloc(2));
-  CPFIT_CUDA(cudaMemsetAsync(bad.ptr, 0xff, 2 * sizeof(unsigned long long), s));
-  SolveParams<T> p{};
-  p.rank = rank;
-  p.dim = dim;
-  p.gram = gram;
-  p.rhs = rhs;
-  p.offsets = L.offsets;
-  p.reg = reg;
-  p.x = x;
-  p.bad = bad.ptr;
+static int launch_solve_smem(const SolveParams<T> &p, int rank, int64_t nrows, cudaStream_t s) {
   const size_t per_warp = (size_t)rank * (rank + 1) * sizeof(double);
   int wpb = (int)(49152 / per_warp);
   if (wpb > 8) wpb = 8;
   if (wpb < 1) wpb = 1;
   const size_t smem = per_warp * wpb;
-  int64_t blocks = (dim + wpb - 1) / wpb;
+  int64_t blocks = (nrows + wpb - 1) / wpb;
   int64_t cap = (int64_t)num_sms() * 16;
   unsigned grid = (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
   const int kb = (rank + 31) / 32;
@@ -530,9 +680,56 @@ static int run_solve(cpfit_pattern *pt, int mode, int rank, const T *gram, const
   }
 #undef CPFIT_SOLVE_CASE
   CPFIT_LAUNCH_CHECK("solve_kernel");
-  unsigned long long h[2];
-  CPFIT_CUDA(cudaMemcpyAsync(h, bad.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
-  CPFIT_CUDA(cudaStreamSynchronize(s));
+  return CPFIT_OK;
+}
+
+template <typename T>
+static int run_solve(cpfit_pattern *pt, int mode, int rank, const T *gram, const T *rhs,
+                     double reg, T *x, int64_t *bad_row, cudaStream_t s) {
+  CpfitModeLayout &L = pt->modes[mode];
+  const int64_t dim = pt->dims[mode];
+  Scratch<unsigned long long> bad(s);
+  CPFIT_TRY(bad.alloc(3));
+  CPFIT_CUDA(cudaMemsetAsync(bad.ptr, 0xff, 2 * sizeof(unsigned long long), s));
+  CPFIT_CUDA(cudaMemsetAsync(bad.ptr + 2, 0, sizeof(unsigned long long), s));
+  SolveParams<T> p{};
+  p.rank = rank;
+  p.dim = dim;
+  p.gram = gram;
+  p.rhs = rhs;
+  p.offsets = L.offsets;
+  p.reg = reg;
+  p.x = x;
+  p.bad = bad.ptr;
+  Scratch<int32_t> retry(s);
+  unsigned long long h[3] = {~0ull, ~0ull, 0};
+  if (rank <= 32) {
+    CPFIT_TRY(retry.alloc(dim > 0 ? dim : 1));
+    p.retry = retry.ptr;
+    p.nretry = bad.ptr + 2;
+    const unsigned grid = (unsigned)((dim + 3) / 4 > 0 ? (dim + 3) / 4 : 1);
+    if (rank <= 8)
+      solve_reg_kernel<T, 8><<<grid, 128, 0, s>>>(p);
+    else if (rank <= 16)
+      solve_reg_kernel<T, 16><<<grid, 128, 0, s>>>(p);
+    else
+      solve_reg_kernel<T, 32><<<grid, 128, 0, s>>>(p);
+    CPFIT_LAUNCH_CHECK("solve_reg_kernel");
+    CPFIT_CUDA(cudaMemcpyAsync(h, bad.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CPFIT_CUDA(cudaStreamSynchronize(s));
+    if (h[2] > 0) {  // rows that are not numerically SPD: Cholesky/LU smem path
+      p.rows = retry.ptr;
+      p.nrows = (int64_t)h[2];
+      CPFIT_TRY(launch_solve_smem<T>(p, rank, p.nrows, s));
+    }
+  } else {
+    CPFIT_TRY(launch_solve_smem<T>(p, rank, dim, s));
+  }
+  if (rank > 32 || h[2] > 0) {
+    CPFIT_CUDA(cudaMemcpyAsync(h, bad.ptr, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
+    CPFIT_CUDA(cudaStreamSynchronize(s));
+  }
   if (h[0] != ~0ull) {
     *bad_row = (int64_t)h[0];
     set_error("mode %d row %lld: no incident entries and reg=0 but right-hand side is nonzero",
