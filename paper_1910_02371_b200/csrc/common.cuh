@@ -169,6 +169,7 @@ struct CpfitModeLayout {
   int32_t *split_row = nullptr;   // nsplit
   int32_t *split_slot = nullptr;  // nsplit + 1
   int32_t *identity_perm = nullptr;  // materialised on request for mode 0
+  bool borrowed = false;  // coarse task tables borrow perm / offsets / sorted_idx
 };
 
 struct cpfit_pattern {
@@ -179,8 +180,14 @@ struct cpfit_pattern {
   int64_t task_size = 1024;
   CpfitModeLayout modes[CPFIT_MAXN];
   int32_t *parent = nullptr;  // sampled patterns: entry -> entry of the source pattern
+  // coarse task tables (task_size * CPFIT_COARSE_TASKS) for the Gram kernel:
+  // fewer split rows, less partial-Gram traffic
+  CpfitModeLayout coarse[CPFIT_MAXN];
 };
+
+#define CPFIT_COARSE_TASKS 8
 
 namespace cpfit {
 int ensure_layout(cpfit_pattern *p, int mode, cudaStream_t s);
+int ensure_coarse_layout(cpfit_pattern *p, int mode, cudaStream_t s);
 }

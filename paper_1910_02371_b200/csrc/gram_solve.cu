@@ -293,8 +293,8 @@ static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
   }
   CPFIT_CUDA(cudaMemsetAsync(gram, 0, (size_t)dim * rr * sizeof(T), s));
   if (pt->nnz == 0) return CPFIT_OK;
-  CPFIT_TRY(ensure_layout(pt, mode, s));
-  CpfitModeLayout &L = pt->modes[mode];
+  CPFIT_TRY(ensure_coarse_layout(pt, mode, s));
+  CpfitModeLayout &L = pt->coarse[mode];
   GramParams<T> p{};
   p.rank = rank;
   int np = 0;
@@ -326,7 +326,7 @@ static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
   CPFIT_TRY(launch_gram<T>(p, s));
   if (L.nsplit > 0) {
     unsigned grid = (unsigned)(L.nsplit < 65535 ? L.nsplit : 65535);
-    combine_gram_partials<T><<<grid, 128, 0, s>>>(L.split_row, L.split_slot, L.nsplit, rr,
+    combine_gram_partials<T><<<grid, 256, 0, s>>>(L.split_row, L.split_slot, L.nsplit, rr,
                                                   partial.ptr, gram);
     CPFIT_LAUNCH_CHECK("combine_gram_partials");
   }
@@ -379,76 +379,93 @@ __device__ __forceinline__ void solve_empty_row(const SolveParams<T> &p, int64_t
 // the trailing update to their own column.  Back substitution: lane k owns
 // L[:, k], so x_k needs one dot product on lane k and one broadcast.
 template <typename T, int RMAX>
-__device__ __forceinline__ bool chol_solve_row(const T *__restrict__ Gr, const T *__restrict__ rh,
-                                               int R, double reg, T *__restrict__ xo) {
+__device__ __forceinline__ void chol_factor_solve(const T *__restrict__ Gr,
+                                                  const T *__restrict__ rh, int R, double reg,
+                                                  double &mine_out, bool &ok_out) {
+  // The R x R system is embedded in an RMAX x RMAX one padded with the
+  // identity (block diagonal: same solution), so every loop below is
+  // guard-free and every shuffle is warp-uniform.
   const int lane = threadIdx.x & 31;
   double a[RMAX], b[RMAX];
 #pragma unroll
   for (int i = 0; i < RMAX; ++i) {
-    a[i] = (i < R && lane < R) ? (double)__ldg(Gr + lane * R + i) : 0.0;
+    const bool in = i < R && lane < R;
+    a[i] = in ? (double)__ldg(Gr + lane * R + i) + (i == lane ? reg : 0.0)
+              : (i == lane ? 1.0 : 0.0);
     b[i] = i < R ? (double)__ldg(rh + i) : 0.0;
-    if (i == lane) a[i] += reg;
   }
   bool ok = true;
+  double my_inv = 1.0;  // 1 / L[lane][lane]
 #pragma unroll
   for (int k = 0; k < RMAX; ++k) {
-    if (k < R) {
-      const double d = __shfl_sync(0xffffffffu, a[k], k);
-      if (!(d > 0.0) || !(d < DBL_MAX)) ok = false;
-      const double lkk = sqrt(d);
-      const double inv = 1.0 / lkk;
-      const double yk = b[k] * inv;
-      double ljk = 0.0;
+    const double d = __shfl_sync(0xffffffffu, a[k], k);
+    ok = ok && (d > 0.0) && (d < DBL_MAX);
+    const double lkk = sqrt(d);
+    const double inv = 1.0 / lkk;
+    const double yk = b[k] * inv;
+    double ljk = 0.0;
 #pragma unroll
-      for (int i = k + 1; i < RMAX; ++i) {
-        if (i < R) {
-          const double ci = __shfl_sync(0xffffffffu, a[i], k) * inv;  // L[i][k]
-          if (i == lane) ljk = ci;
-          a[i] = lane == k ? ci : (lane > k ? fma(-ci, ljk, a[i]) : a[i]);
-          b[i] = fma(-ci, yk, b[i]);  // forward substitution, replicated
-        }
-      }
-      if (lane == k) a[k] = lkk;
-      b[k] = yk;
+    for (int i = k + 1; i < RMAX; ++i) {
+      const double ci = __shfl_sync(0xffffffffu, a[i], k) * inv;  // L[i][k]
+      ljk = (i == lane) ? ci : ljk;                              // L[lane][k] once i == lane
+      a[i] = fma(-ci, ljk, a[i]);  // trailing update (no-op while ljk == 0)
+      b[i] = fma(-ci, yk, b[i]);   // forward substitution, replicated in every lane
     }
+    const double m = lane == k ? inv : 1.0;  // lane k: column k becomes L[:, k]
+#pragma unroll
+    for (int i = k + 1; i < RMAX; ++i) a[i] *= m;
+    if (lane == k) {
+      a[k] = lkk;
+      my_inv = inv;
+    }
+    b[k] = yk;
   }
-  // back substitution L^T x = y (harmless garbage when !ok: not stored)
+  // back substitution L^T x = y: lane k owns L[:, k] (garbage when !ok, not stored)
 #pragma unroll
   for (int kk = 0; kk < RMAX; ++kk) {
     const int k = RMAX - 1 - kk;
-    if (k < R) {
-      double sdot = 0.0;
+    double sdot = 0.0;
 #pragma unroll
-      for (int i = k + 1; i < RMAX; ++i)
-        if (i < R) sdot = fma(a[i], b[i], sdot);
-      b[k] = __shfl_sync(0xffffffffu, (b[k] - sdot) / a[k], k);
-    }
+    for (int i = k + 1; i < RMAX; ++i) sdot = fma(a[i], b[i], sdot);
+    b[k] = __shfl_sync(0xffffffffu, (b[k] - sdot) * my_inv, k);
   }
   double mine = 0.0;
 #pragma unroll
   for (int i = 0; i < RMAX; ++i)
     if (i == lane) mine = b[i];
-  if (!__all_sync(0xffffffffu, ok)) return false;
-  if (lane < R) xo[lane] = (T)mine;
-  return true;
+  mine_out = mine;
+  ok_out = __all_sync(0xffffffffu, ok);
 }
 
-// One warp per row and no grid-stride loop: inside a loop ptxas keeps the
-// fully unrolled register arrays on the stack.
+// One warp per row and no grid-stride loop (inside a loop ptxas keeps the
+// fully unrolled register arrays on the stack); the Cholesky runs
+// unconditionally so its shuffles sit in convergent code (no divergence
+// fallback paths), results are used only for active, non-empty rows.
+template <typename T, int RMAX>
+__device__ __forceinline__ void chol_factor_solve(const T *__restrict__ Gr,
+                                                  const T *__restrict__ rh, int R, double reg,
+                                                  double &mine, bool &ok);
+
 template <typename T, int RMAX>
 __global__ void __launch_bounds__(128) solve_reg_kernel(const SolveParams<T> p) {
   const int lane = threadIdx.x & 31;
   const int R = p.rank;
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (row >= p.dim) return;
-  if (p.offsets[row + 1] == p.offsets[row]) {
+  const int64_t wrow = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const bool active = wrow < p.dim;
+  const int64_t row = active ? wrow : p.dim - 1;
+  const bool empty = p.offsets[row + 1] == p.offsets[row];
+  double mine;
+  bool ok;
+  chol_factor_solve<T, RMAX>(p.gram + row * (int64_t)R * R, p.rhs + row * (int64_t)R, R, p.reg,
+                             mine, ok);
+  if (!active) return;
+  if (empty) {
     solve_empty_row(p, row);
-  } else if (!chol_solve_row<T, RMAX>(p.gram + row * (int64_t)R * R, p.rhs + row * (int64_t)R,
-                                      R, p.reg, p.x + row * (int64_t)R)) {
-    if (lane == 0) {
-      const unsigned long long slot = atomicAdd(p.nretry, 1ull);
-      p.retry[slot] = (int32_t)row;
-    }
+  } else if (ok) {
+    if (lane < R) p.x[row * (int64_t)R + lane] = (T)mine;
+  } else if (lane == 0) {
+    const unsigned long long slot = atomicAdd(p.nretry, 1ull);
+    p.retry[slot] = (int32_t)row;
   }
 }
 

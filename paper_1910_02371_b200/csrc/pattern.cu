@@ -443,6 +443,23 @@ int ensure_layout(cpfit_pattern *p, int mode, cudaStream_t s) {
   return CPFIT_OK;
 }
 
+int ensure_coarse_layout(cpfit_pattern *p, int mode, cudaStream_t s) {
+  CPFIT_TRY(ensure_layout(p, mode, s));
+  CpfitModeLayout &C = p->coarse[mode];
+  if (C.built) return CPFIT_OK;
+  const CpfitModeLayout &L = p->modes[mode];
+  C.perm = L.perm;
+  C.offsets = L.offsets;
+  for (int k = 0; k < p->order; ++k) {
+    C.sorted_idx[k] = L.sorted_idx[k];
+    C.owns_sorted[k] = false;
+  }
+  C.borrowed = true;
+  CPFIT_TRY(build_tasks(C, p->dims[mode], p->nnz, p->task_size * CPFIT_COARSE_TASKS, s));
+  C.built = true;
+  return CPFIT_OK;
+}
+
 template <typename T>
 static int permute_vals(const T *in, const int32_t *perm, T *out, int64_t n, cudaStream_t s) {
   if (n <= 0) return CPFIT_OK;
@@ -551,6 +568,12 @@ int cpfit_pattern_destroy(cpfit_pattern *p) {
     if (L.split_row) cudaFree(L.split_row);
     if (L.split_slot) cudaFree(L.split_slot);
     if (L.identity_perm) cudaFree(L.identity_perm);
+    CpfitModeLayout &C = p->coarse[m];
+    if (C.task_begin) cudaFree(C.task_begin);
+    if (C.task_row) cudaFree(C.task_row);
+    if (C.task_slot) cudaFree(C.task_slot);
+    if (C.split_row) cudaFree(C.split_row);
+    if (C.split_slot) cudaFree(C.split_slot);
   }
   for (int n = 0; n < p->order; ++n)
     if (p->coords[n]) cudaFree(p->coords[n]);
