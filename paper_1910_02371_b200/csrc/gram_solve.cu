@@ -175,25 +175,49 @@ gram_kernel(const GramParams<T> p) {
       }
       __syncwarp();
     }
-    // store the tiles (and their mirror images) as rows of G
+    // store G (tiles and their mirror images)
     const int slot = p.task_slot[t];
     T *dst = slot < 0 ? p.gram + (int64_t)p.task_row[t] * rank * rank
                       : p.partial + (int64_t)slot * rank * rank;
-    int tile = 0;
+    if constexpr (RP <= GRAM_CHUNK) {
+      // transpose through the staging buffer, then write whole rows coalesced
+      int tile = 0;
 #pragma unroll
-    for (int i = 0; i < RT; ++i)
+      for (int i = 0; i < RT; ++i)
 #pragma unroll
-      for (int jt = i; jt < RT; ++jt) {
+        for (int jt = i; jt < RT; ++jt) {
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int r = 8 * i + gq, c = 8 * jt + 2 * tq + v;
-          if (r < rank && c < rank) {
-            dst[(int64_t)r * rank + c] = (T)acc[tile][v];
-            if (i != jt) dst[(int64_t)c * rank + r] = (T)acc[tile][v];
+          for (int v = 0; v < 2; ++v) {
+            const int r = 8 * i + gq, c = 8 * jt + 2 * tq + v;
+            H[r * LD + c] = acc[tile][v];
+            H[c * LD + r] = acc[tile][v];
           }
+          ++tile;
         }
-        ++tile;
+      __syncwarp();
+      const int total = rank * rank;
+      for (int k = lane; k < total; k += 32) {
+        const int r = k / rank, c = k - r * rank;
+        dst[k] = (T)H[r * LD + c];
       }
+      __syncwarp();
+    } else {
+      int tile = 0;
+#pragma unroll
+      for (int i = 0; i < RT; ++i)
+#pragma unroll
+        for (int jt = i; jt < RT; ++jt) {
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int r = 8 * i + gq, c = 8 * jt + 2 * tq + v;
+            if (r < rank && c < rank) {
+              dst[(int64_t)r * rank + c] = (T)acc[tile][v];
+              if (i != jt) dst[(int64_t)c * rank + r] = (T)acc[tile][v];
+            }
+          }
+          ++tile;
+        }
+    }
   }
 }
 
@@ -233,8 +257,15 @@ static int launch_gram_v(const GramParams<T> &p, cudaStream_t s) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
+  // persistent grid: exactly the resident capacity
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gram_kernel<T, RT, VEC, NPT>,
+                                                  GRAM_WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
   int64_t blocks = (p.ntasks + GRAM_WARPS - 1) / GRAM_WARPS;
-  int64_t cap = (int64_t)num_sms() * 8;
+  int64_t cap = (int64_t)num_sms() * per_sm;
   unsigned grid = (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
   gram_kernel<T, RT, VEC, NPT><<<grid, GRAM_WARPS * 32, smem, s>>>(p);
   CPFIT_LAUNCH_CHECK("gram_kernel");

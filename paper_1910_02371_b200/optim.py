@@ -232,13 +232,14 @@ def _als_mode_device(t: SparseTensor, F, mode: int, reg: float, keep_gram: bool 
     else:
         rhs.zero_()
     x = torch.empty_like(rhs)
-    gram = torch.empty((t.shape[mode], rank, rank), dtype=dtype, device=dev) \
-        if keep_gram else None
+    # always a torch-cached buffer: a library-side scratch of I_n x R x R would
+    # hit the stream-ordered pool's allocate/release path on every call
+    gram = torch.empty((t.shape[mode], rank, rank), dtype=dtype, device=dev)
     bad = ctypes.c_int64(-1)
     st = L.cpfit_solve_factor(pat.handle, mode, code, rank, None, 1, ptrs,
                               ctypes.c_void_p(rhs.data_ptr()), float(reg),
                               ctypes.c_void_p(x.data_ptr()),
-                              ctypes.c_void_p(0 if gram is None else gram.data_ptr()),
+                              ctypes.c_void_p(gram.data_ptr()),
                               ctypes.byref(bad), _stream())
     if st == _lib.EEMPTYROW:
         raise NumericalError(
