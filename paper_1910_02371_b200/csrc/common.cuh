@@ -42,11 +42,12 @@ inline int num_sms() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
-    // keep up to 4 GB of freed scratch in the stream-ordered pool instead of
-    // returning it to the driver at every synchronisation
+    // optionally keep freed scratch in the stream-ordered pool (CPFIT_POOL_KEEP_GB;
+    // default 0: measured slower on cfg 3 ALS when competing with torch's cache)
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = 4ull << 30;
+      const char *env = getenv("CPFIT_POOL_KEEP_GB");
+      uint64_t keep = (uint64_t)(env ? atoi(env) : 0) << 30;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }
