@@ -182,6 +182,27 @@ int cpfit_ccd_update(cpfit_pattern *p, int mode, const double *const *cols,
                      const double *old_col, double *new_col, double *resid,
                      double reg, void *stream);
 
+/* Batched regularised SPD solves without a tensor pattern:
+ * (G_i + reg I) x_i = rhs_i for i < nrows, G_i = gram + i * gram_stride
+ * (gram_stride 0: one shared G, e.g. the dense CP-ALS Gram (B^T B)*(C^T C)).
+ * Same kernels and singular-row semantics as cpfit_solve_factor. */
+int cpfit_solve_rows(int dtype, int rank, int64_t nrows, const void *gram,
+                     int64_t gram_stride, const void *rhs, double reg,
+                     void *x_out, int64_t *bad_row, void *stream);
+
+/* ---- dense tensors (BASELINE cfg 4; no reference counterpart: its oracle
+ * is kernels.mttkrp on a fully observed tensor, kernels.py:46-91) -------- */
+
+/* axis 1: out[i, r] = sum_j T[i, j, r] W[j, r]   (out I x R)
+ * axis 0: out[j, r] = sum_i T[i, j, r] W[i, r]   (out J x R)
+ * Epilogue of the dense MTTKRP after the plain GEMM T = X_(IJ x K) C. */
+int cpfit_dense_reduce(int dtype, int64_t I, int64_t J, int rank, const void *T,
+                       const void *W, int axis, void *out, void *stream);
+
+/* out[(i*J + j), r] = A[i, r] * B[j, r]  (Khatri-Rao product, IJ x R). */
+int cpfit_khatri_rao(int dtype, int64_t I, int64_t J, int rank, const void *A,
+                     const void *B, void *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,6 +35,7 @@ SYMBOLS = (
     "cpfit_tttp", "cpfit_mttkrp", "cpfit_gram", "cpfit_solve_factor",
     "cpfit_tttp_axpby", "cpfit_sample", "cpfit_pattern_parent_index", "cpfit_gather_values",
     "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_update", "cpfit_probe_gather",
+    "cpfit_solve_rows", "cpfit_dense_reduce", "cpfit_khatri_rao",
 )
 
 _vp = ctypes.c_void_p
@@ -90,6 +91,10 @@ def load(path: str | None = None):
                              ctypes.POINTER(_int), _vp],
         "cpfit_ccd_update": [_vp, _int, _PP, _vp, _vp, _vp, ctypes.c_double, _vp],
         "cpfit_probe_gather": [_vp, _int, _int, _PP, _i64, _vp, _i64, _vp],
+        "cpfit_solve_rows": [_int, _int, _i64, _vp, _i64, _vp, ctypes.c_double, _vp,
+                             ctypes.POINTER(_i64), _vp],
+        "cpfit_dense_reduce": [_int, _i64, _i64, _int, _vp, _vp, _int, _vp, _vp],
+        "cpfit_khatri_rao": [_int, _i64, _i64, _int, _vp, _vp, _vp, _vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

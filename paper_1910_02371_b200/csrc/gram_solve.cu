@@ -379,6 +379,7 @@ struct SolveParams {
   unsigned long long *bad;  // [0] first empty row with nonzero rhs, [1] first singular row
   const int32_t *rows;      // smem kernel: explicit row list (null: rows 0..dim-1)
   int64_t nrows;
+  int64_t gstride;          // elements between consecutive rows' G (0: one shared G)
   int32_t *retry;           // register kernel: rows whose Cholesky failed
   unsigned long long *nretry;
 };
@@ -484,10 +485,10 @@ __global__ void __launch_bounds__(128) solve_reg_kernel(const SolveParams<T> p) 
   const int64_t wrow = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const bool active = wrow < p.dim;
   const int64_t row = active ? wrow : p.dim - 1;
-  const bool empty = p.offsets[row + 1] == p.offsets[row];
+  const bool empty = p.offsets ? p.offsets[row + 1] == p.offsets[row] : false;
   double mine;
   bool ok;
-  chol_factor_solve<T, RMAX>(p.gram + row * (int64_t)R * R, p.rhs + row * (int64_t)R, R, p.reg,
+  chol_factor_solve<T, RMAX>(p.gram + row * p.gstride, p.rhs + row * (int64_t)R, R, p.reg,
                              mine, ok);
   if (!active) return;
   if (empty) {
@@ -594,7 +595,7 @@ __global__ void solve_kernel(const SolveParams<T> p, int warps_per_block) {
   const int64_t nrows = p.rows ? p.nrows : p.dim;
   for (int64_t it = warp; it < nrows; it += nwarps) {
     const int64_t row = p.rows ? (int64_t)p.rows[it] : it;
-    const bool empty = p.offsets[row + 1] == p.offsets[row];
+    const bool empty = p.offsets ? p.offsets[row + 1] == p.offsets[row] : false;
     const T *rhs = p.rhs + row * R;
     T *xo = p.x + row * R;
     double b[KB];
@@ -621,7 +622,7 @@ __global__ void solve_kernel(const SolveParams<T> p, int warps_per_block) {
       if (__any_sync(0xffffffffu, nz) && lane == 0) atomicMin(&p.bad[0], (unsigned long long)row);
       continue;
     }
-    const T *G = p.gram + row * R * R;
+    const T *G = p.gram + row * p.gstride;
     for (int q = lane; q < R * R; q += 32) {
       int i = q / R, j = q % R;
       A[i * ld + j] = (double)G[q] + (i == j ? p.reg : 0.0);
@@ -732,10 +733,9 @@ static int launch_solve_smem(const SolveParams<T> &p, int rank, int64_t nrows, c
 }
 
 template <typename T>
-static int run_solve(cpfit_pattern *pt, int mode, int rank, const T *gram, const T *rhs,
-                     double reg, T *x, int64_t *bad_row, cudaStream_t s) {
-  CpfitModeLayout &L = pt->modes[mode];
-  const int64_t dim = pt->dims[mode];
+static int run_solve_rows(int mode, int64_t dim, const int64_t *offsets, int rank, const T *gram,
+                          int64_t gstride, const T *rhs, double reg, T *x, int64_t *bad_row,
+                          cudaStream_t s) {
   Scratch<unsigned long long> bad(s);
   CPFIT_TRY(bad.alloc(3));
   CPFIT_CUDA(cudaMemsetAsync(bad.ptr, 0xff, 2 * sizeof(unsigned long long), s));
@@ -745,7 +745,8 @@ static int run_solve(cpfit_pattern *pt, int mode, int rank, const T *gram, const
   p.dim = dim;
   p.gram = gram;
   p.rhs = rhs;
-  p.offsets = L.offsets;
+  p.offsets = offsets;
+  p.gstride = gstride;
   p.reg = reg;
   p.x = x;
   p.bad = bad.ptr;
@@ -794,6 +795,13 @@ static int run_solve(cpfit_pattern *pt, int mode, int rank, const T *gram, const
 }
 
 template <typename T>
+static int run_solve(cpfit_pattern *pt, int mode, int rank, const T *gram, const T *rhs,
+                     double reg, T *x, int64_t *bad_row, cudaStream_t s) {
+  return run_solve_rows<T>(mode, pt->dims[mode], pt->modes[mode].offsets, rank, gram,
+                           (int64_t)rank * rank, rhs, reg, x, bad_row, s);
+}
+
+template <typename T>
 static int run_solve_factor(cpfit_pattern *pt, int mode, int rank, const void *weights,
                             int weights_sorted, const void *const *factors, const void *rhs,
                             double reg, void *x_out, void *gram_out, int64_t *bad_row,
@@ -838,6 +846,31 @@ int cpfit_gram(cpfit_pattern *p, int mode, int dtype, int rank, const void *weig
   if (dtype == CPFIT_F32)
     return run_gram<float>(p, mode, rank, (const float *)weights, weights_sorted, factors,
                            (float *)gram_out, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+int cpfit_solve_rows(int dtype, int rank, int64_t nrows, const void *gram, int64_t gram_stride,
+                     const void *rhs, double reg, void *x_out, int64_t *bad_row, void *stream) {
+  if (rank < 1 || nrows < 0 || gram_stride < 0) {
+    set_error("invalid solve_rows arguments");
+    return CPFIT_EINVAL;
+  }
+  if (reg < 0.0) {
+    set_error("regularization must be >= 0");
+    return CPFIT_EINVAL;
+  }
+  if (nrows == 0) return CPFIT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t dummy = -1;
+  if (dtype == CPFIT_F64)
+    return run_solve_rows<double>(-1, nrows, nullptr, rank, (const double *)gram, gram_stride,
+                                  (const double *)rhs, reg, (double *)x_out,
+                                  bad_row ? bad_row : &dummy, s);
+  if (dtype == CPFIT_F32)
+    return run_solve_rows<float>(-1, nrows, nullptr, rank, (const float *)gram, gram_stride,
+                                 (const float *)rhs, reg, (float *)x_out,
+                                 bad_row ? bad_row : &dummy, s);
   set_error("unknown dtype %d", dtype);
   return CPFIT_EINVAL;
 }
