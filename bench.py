@@ -302,6 +302,53 @@ def als_section(world, rank, dev, sweeps=2):
     return out
 
 
+CPU_DENSE_EINSUM_S = [1.80, 0.44, 0.47]  # host numpy.einsum per mode, 8 vCPU
+
+
+def dense_section(dev, sweeps=2):
+    """BASELINE cfg 4: dense 800^3 fp64 N(0,1), R=64 factors N(0,1): dense
+    MTTKRP per mode and CP-ALS sweep time, against the on-box DGEMM peak."""
+    import torch
+
+    from paper_1910_02371_b200 import dense as DN
+    g = torch.Generator(device=dev)
+    g.manual_seed(4)
+    n, R4 = 800, 64
+    X = torch.randn((n, n, n), generator=g, dtype=torch.float64, device=dev)
+    F = [torch.randn((n, R4), generator=g, dtype=torch.float64, device=dev) for _ in range(3)]
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    flop = 2.0 * n ** 3 * R4
+    mode_ms = [timed(lambda m=m: DN.dense_mttkrp(X, F, m)) for m in range(3)]
+    a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    peak_ms = timed(lambda: a @ a)
+    peak = 2 * 8192 ** 3 / (peak_ms * 1e-3) / 1e12
+    del a
+    Fs = [f.clone() for f in F]
+    sweep_ms = timed(lambda: DN.dense_als_sweep(X, Fs, 1e-5), reps=sweeps)
+    return {"workload": "BASELINE cfg 4: dense 800^3 fp64 N(0,1), R=64, lambda=1e-5",
+            "mttkrp_ms": mode_ms,
+            "mttkrp_tflops": [flop / (t * 1e-3) / 1e12 for t in mode_ms],
+            "dgemm_peak_tflops_measured": peak,
+            "mttkrp_frac_of_dgemm_peak": [flop / (t * 1e-3) / 1e12 / peak for t in mode_ms],
+            "als_sweep_ms": sweep_ms,
+            "als_sweep_flop_model": "2 GEMMs per sweep (X*C shared by modes 0,1; X^T*KR(A,B))",
+            "cpu_numpy_einsum_s_per_mode": CPU_DENSE_EINSUM_S,
+            "cpu_note": "host numpy.einsum(optimize=True), 8 vCPU survey container "
+                        "(the reference has no dense path)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -311,6 +358,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-als", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -506,6 +554,13 @@ def main():
             als = als_section(world, rank, dev)
         except Exception as exc:  # reported, never fatal to the headline line
             als = {"error": repr(exc)}
+    dense = None
+    if not args.no_dense and world == 1:
+        torch.cuda.empty_cache()
+        try:
+            dense = dense_section(dev)
+        except Exception as exc:
+            dense = {"error": repr(exc)}
 
     if rank == 0:
         line = {
@@ -517,7 +572,7 @@ def main():
             "roofline": roofline, "kernels": kernels, "gather_ceiling": probe,
             "compulsory_bytes_per_pass": compulsory,
             "clocks": clk, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
-            "als": als,
+            "als": als, "dense": dense,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample()
