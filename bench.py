@@ -303,6 +303,59 @@ def als_section(world, rank, dev, sweeps=2):
 
 
 CPU_DENSE_EINSUM_S = [1.80, 0.44, 0.47]  # host numpy.einsum per mode, 8 vCPU
+CPU_CFG5_SCALED = {"tttp_s_at_1e7": 3.56, "sgd_step_s_at_1e7": 1.11}  # SURVEY.md 6, f64 numpy
+
+
+def sgd_section(dev, steps=5):
+    """BASELINE cfg 5 on one GPU: order-4 fp32 tensor 1e5^3 x 1e3 with 1e9
+    distinct uniform nonzeros (device-generated, values = rank-8 CP model +
+    N(0, 0.1) via the library's TTTP), R=64: SGD steps (1% Bernoulli sample,
+    step 1e-3, lambda 1e-4) and the full TTTP residual evaluation."""
+    import torch
+
+    import paper_1910_02371_b200 as cp
+    from paper_1910_02371_b200 import synth
+    from paper_1910_02371_b200.losses import sum_sq, tttp_affine
+    from paper_1910_02371_b200.optim import SolverConfig, _sgd_ls_device
+    t0 = time.perf_counter()
+    shape, tn, values, F = synth.cfg5_device()
+    t = tn.with_values(values)
+    gen_s = time.perf_counter() - t0
+    cfg = SolverConfig(rank=64, algorithm="sgd", step=1e-3, reg=1e-4, sample_rate=0.01)
+    stream = torch.cuda.current_stream()
+    root = cp.RngState(5).child(1)
+    _sgd_ls_device(t, F, cfg, root.child(0))  # warm-up
+    torch.cuda.synchronize()
+    ms, kept = [], []
+    for it in range(1, steps + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        kept.append(_sgd_ls_device(t, F, cfg, root.child(it)))
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    resid = tttp_affine(t, F, -1.0, 1.0, torch.float32)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    resid = tttp_affine(t, F, -1.0, 1.0, torch.float32)
+    b.record(stream)
+    torch.cuda.synchronize()
+    tttp_ms = a.elapsed_time(b)
+    rmse = float(np.sqrt(sum_sq(resid) / t.nnz))
+    alg = t.nnz * (4 * 4 + 2 * 4 + 4 * 64 * 4)  # SURVEY 8d: 1,048 B per nnz
+    return {"workload": "BASELINE cfg 5: order 4, 1e5x1e5x1e5x1e3, 1e9 uniform distinct nnz, "
+                        "fp32, R=64; SGD rate 0.01 (Bernoulli), step 1e-3, lambda 1e-4",
+            "generation_s": gen_s, "nnz": t.nnz,
+            "sgd_step_ms": float(np.mean(ms)), "sample_nnz_per_step": float(np.mean(kept)),
+            "tttp_residual_ms": tttp_ms,
+            "tttp_residual_nnz_per_s": t.nnz / (tttp_ms * 1e-3),
+            "tttp_residual_alg_gbs": alg / (tttp_ms * 1e-3) / 1e9,
+            "rmse_after": rmse,
+            "cpu_reference_scaled": {"tttp_s": CPU_CFG5_SCALED["tttp_s_at_1e7"] * 100,
+                                     "sgd_step_s": CPU_CFG5_SCALED["sgd_step_s_at_1e7"] * 100,
+                                     "note": "reference f64 numpy path at 1e7 nnz x 100 "
+                                             "(1e9 does not fit the reference host; SURVEY 8d)"}}
 
 
 def dense_section(dev, sweeps=2):
@@ -359,6 +412,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-als", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-sgd", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -561,6 +615,14 @@ def main():
             dense = dense_section(dev)
         except Exception as exc:
             dense = {"error": repr(exc)}
+    sgd = None
+    if not args.no_sgd and world == 1:
+        torch.cuda.empty_cache()
+        try:
+            sgd = sgd_section(dev)
+        except Exception as exc:
+            sgd = {"error": repr(exc)}
+        torch.cuda.empty_cache()
 
     if rank == 0:
         line = {
@@ -572,7 +634,7 @@ def main():
             "roofline": roofline, "kernels": kernels, "gather_ceiling": probe,
             "compulsory_bytes_per_pass": compulsory,
             "clocks": clk, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
-            "als": als, "dense": dense,
+            "als": als, "dense": dense, "sgd": sgd,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample()

@@ -174,3 +174,36 @@ def cfg3_device(seed: int = CFG3_SEED, nnz: int = 100_480_507,
         keys = keys[torch.sort(pick).values]
     values = torch.randint(1, 6, (nnz,), generator=g, device=device).to(torch.float64)
     return shape, keys, values
+
+
+def cfg5_device(seed: int = CFG5_SEED, nnz: int = 1_000_000_000,
+                shape=(100_000, 100_000, 100_000, 1_000), rank: int = 64, device="cuda"):
+    """BASELINE cfg 5 synthesised on the GPU: order 4, nnz distinct uniform
+    keys, values = rank-8 CP model (truth factors N(0, 1/8), evaluated with
+    the library's own TTTP kernel) + N(0, 0.1) noise, fp32; R=64 factors
+    N(0, 1/R).  Returns (shape, sorted int64 keys, f32 values, f32 factors)."""
+    import torch
+    shape = tuple(int(d) for d in shape)
+    space = 1
+    for d in shape:
+        space *= d
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    keys = torch.unique(torch.randint(0, space, (int(nnz * 1.0001) + 64,), generator=g,
+                                      device=device, dtype=torch.int64))
+    while keys.numel() < nnz:
+        extra = torch.randint(0, space, (2 * (nnz - keys.numel()) + 64,), generator=g,
+                              device=device, dtype=torch.int64)
+        keys = torch.unique(torch.cat([keys, extra]))
+    if keys.numel() > nnz:
+        pick = torch.randperm(keys.numel(), generator=g, device=device)[:nnz]
+        keys = keys[torch.sort(pick).values]
+    truth = [torch.randn((d, 8), generator=g, device=device) * (1.0 / 8) ** 0.5 for d in shape]
+    noise = torch.randn((nnz,), generator=g, device=device) * 0.1
+    factors = [torch.randn((d, rank), generator=g, device=device) * (1.0 / rank) ** 0.5
+               for d in shape]
+    from .core import SparseTensor
+    from .losses import tttp_affine
+    t = SparseTensor.from_device(shape, keys, noise)
+    values = tttp_affine(t, truth, 1.0, 1.0, torch.float32)  # model + noise
+    return shape, t, values, factors
