@@ -218,7 +218,7 @@ CPU_ALS_SURVEY_S = 125.0   # reference ALS sweep, cfg 3 full, 8 vCPU (SURVEY.md 
 CPU_CCD_SURVEY_S = 562.0   # reference CCD++ sweep, same host
 
 
-def als_section(world, rank, dev, sweeps=2):
+def als_section(world, rank, dev, sweeps=3):
     """BASELINE cfg 3 (480,189 x 17,770 x 2,182, 100,480,507 Zipf nnz, R=32,
     lambda=1e-5): device-generated seeded instance; ALS sweep time at N GPUs
     (row-sharded with an NCCL all-gather per mode when N > 1; strong scaling),
@@ -247,6 +247,7 @@ def als_section(world, rank, dev, sweeps=2):
         _als_ls_device(t, F, REG)  # warm-up sweep: builds the mode layouts
         torch.cuda.synchronize()
         out["first_sweep_incl_layout_s"] = time.perf_counter() - t1
+        _als_ls_device(t, F, REG)  # second warm-up: allocator caches settle
         times = []
         for _ in range(sweeps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -255,7 +256,19 @@ def als_section(world, rank, dev, sweeps=2):
             b.record(stream)
             torch.cuda.synchronize()
             times.append(a.elapsed_time(b))
-        out["als_sweep_ms"] = float(np.mean(times))
+        out["als_sweep_ms"] = float(np.median(times))
+        out["als_sweep_ms_all"] = times
+        # per-phase split of one more sweep (MTTKRP rhs vs Gram + solve)
+        from paper_1910_02371_b200.optim import _als_mode_device
+        phases = []
+        for mode in range(3):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            e[0].record(stream)
+            F[mode] = _als_mode_device(t, F, mode, REG)
+            e[1].record(stream)
+            torch.cuda.synchronize()
+            phases.append(e[0].elapsed_time(e[1]))
+        out["als_mode_update_ms"] = phases
         from paper_1910_02371_b200.losses import ls_data_term
         out["rmse_after"] = float(np.sqrt(ls_data_term(t, F) / t.nnz))
         F = [f.clone() for f in init]

@@ -74,15 +74,33 @@ inline void dfree(T *p, cudaStream_t s) {
   if (p) cudaFreeAsync((void *)p, s);
 }
 
-// RAII holder for stream-ordered scratch.
+// Per-call scratch comes from a small stream-keyed cache of power-of-two
+// blocks (pattern.cu): blocks released on stream s are only handed out again
+// on stream s, so reuse is stream-ordered and needs no synchronisation.
+// Keeps the per-sweep kernels off the driver's allocate / map / unmap path.
+void *scratch_get(size_t bytes, cudaStream_t s, size_t *cap);
+void scratch_put(void *p, size_t cap, cudaStream_t s);
+
+// RAII holder for per-call scratch.
 template <typename T>
 struct Scratch {
   T *ptr = nullptr;
+  size_t cap = 0;
   cudaStream_t s = nullptr;
   Scratch() = default;
   explicit Scratch(cudaStream_t st) : s(st) {}
-  int alloc(size_t n) { return dalloc(&ptr, n, s); }
-  ~Scratch() { dfree(ptr, s); }
+  int alloc(size_t n) {
+    if (n == 0) return CPFIT_OK;
+    ptr = (T *)scratch_get(n * sizeof(T), s, &cap);
+    if (!ptr) {
+      set_error("device allocation of %zu bytes failed", n * sizeof(T));
+      return CPFIT_ENOMEM;
+    }
+    return CPFIT_OK;
+  }
+  ~Scratch() {
+    if (ptr) scratch_put(ptr, cap, s);
+  }
   Scratch(const Scratch &) = delete;
   Scratch &operator=(const Scratch &) = delete;
 };

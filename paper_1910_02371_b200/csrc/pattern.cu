@@ -6,7 +6,9 @@
 // (core.py:93-102), counting_sort_by_mode (core.py:234-249).
 #include <cstdarg>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <vector>
 
 #include "common.cuh"
 
@@ -19,6 +21,56 @@ void set_error(const char *fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+// ---------------------------------------------------------------------------
+// scratch cache (see common.cuh)
+
+namespace {
+struct CachedBlock {
+  void *p;
+  size_t cap;
+  cudaStream_t s;
+};
+std::mutex g_scratch_mu;
+std::vector<CachedBlock> g_scratch;
+size_t g_scratch_bytes = 0;
+constexpr size_t kScratchKeep = 2ull << 30;  // bytes kept cached at most
+}  // namespace
+
+void *scratch_get(size_t bytes, cudaStream_t s, size_t *cap) {
+  size_t c = 256;
+  while (c < bytes) c <<= 1;
+  {
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    for (size_t i = 0; i < g_scratch.size(); ++i) {
+      if (g_scratch[i].cap == c && g_scratch[i].s == s) {
+        void *p = g_scratch[i].p;
+        g_scratch_bytes -= c;
+        g_scratch[i] = g_scratch.back();
+        g_scratch.pop_back();
+        *cap = c;
+        return p;
+      }
+    }
+  }
+  void *p = nullptr;
+  if (cudaMallocAsync(&p, c, s) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  *cap = c;
+  return p;
+}
+
+void scratch_put(void *p, size_t cap, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  if (g_scratch_bytes + cap > kScratchKeep) {
+    cudaFreeAsync(p, s);
+    return;
+  }
+  g_scratch.push_back({p, cap, s});
+  g_scratch_bytes += cap;
 }
 
 int cuda_status(cudaError_t e, const char *what) {
