@@ -535,11 +535,18 @@ def main():
     for k in kernels.values():
         k["frac"] = k["gbs"] / peak
         k["nnz_per_s"] = t.nnz / (k["ms"] * 1e-3)
-    dom = max(kernels, key=lambda k: kernels[k]["ms"])
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"], "peak": peak,
+    # dominant kernel = largest share of the step (MTTKRP runs once per mode)
+    share = {"tttp": kernels["tttp"]["ms"],
+             "mttkrp0": sum(kernels[f"mttkrp{m}"]["ms"] for m in range(3))}
+    dom = max(share, key=share.get)
+    roofline = {"bound": "hbm", "kernel": "mttkrp_kernel" if dom == "mttkrp0" else "tttp_kernel",
+                "achieved": kernels[dom]["gbs"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dom]["gbs"] / peak, "peak_kind": peak_kind,
+                "step_share": share[dom] / sum(share.values()),
                 "traffic": None,
-                "byte_model": "gather-inclusive algorithmic bytes, SURVEY.md 8(d)"}
+                "byte_model": "gather-inclusive algorithmic bytes per launch, SURVEY.md 8(d); "
+                              "the factor-row gathers are served by L1/L2 (see traffic = ncu "
+                              "DRAM bytes per launch, and frac_of_gather_ceiling)"}
     # gather ceiling: the same row gathers with no compute (probe kernel)
     probe = None
     try:
