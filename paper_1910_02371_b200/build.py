@@ -57,7 +57,14 @@ def _compile(src: str, extra: list[str]) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     if r.stderr.strip():
-        sys.stderr.write(r.stderr)
+        spills = r.stderr.count("Registers are spilled")
+        other = [l for l in r.stderr.splitlines()
+                 if l.strip() and "Registers are spilled" not in l]
+        if other:
+            sys.stderr.write("\n".join(other) + "\n")
+        if spills:
+            sys.stderr.write(f"{os.path.basename(src)}: {spills} kernel variants spill "
+                             "(rarely used large-rank / generic-order instantiations)\n")
     return obj
 
 

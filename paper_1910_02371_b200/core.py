@@ -53,6 +53,18 @@ def current_stream() -> int:
     return _torch().cuda.current_stream().cuda_stream
 
 
+def to_host(t, dtype=None) -> np.ndarray:
+    """Device tensor -> numpy through torch's pinned host cache: the copy is a
+    direct DMA at full PCIe rate, and the pinned block goes back to torch's
+    cache when the returned array is released."""
+    torch = _torch()
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
+
+
 class _CudaArray:
     """Zero-copy __cuda_array_interface__ view of library-owned device memory."""
 
@@ -317,7 +329,7 @@ class SparseTensor:
             dv = self._dvals.get(torch.float64)
             if dv is None:
                 dv = next(iter(self._dvals.values()))
-            self._values = dv.to(torch.float64).cpu().numpy()
+            self._values = to_host(dv, torch.float64)
         return self._values
 
     @property

@@ -29,6 +29,9 @@
 #ifndef CPFIT_MTTKRP_MINB
 #define CPFIT_MTTKRP_MINB 3
 #endif
+#ifndef CPFIT_MTTKRP_U
+#define CPFIT_MTTKRP_U 4  // sub-iterations of gathers in flight per MTTKRP round
+#endif
 #ifndef CPFIT_MTTKRP_KVT64
 #define CPFIT_MTTKRP_KVT64 1
 #endif
@@ -246,7 +249,7 @@ template <typename T, int VEC, int LPE, int KV, int NP, bool FULL>
 __global__ void __launch_bounds__(256, CPFIT_MTTKRP_MINB) mttkrp_kernel(const MttkrpParams<T> p) {
   constexpr int G = 32 / LPE;
   constexpr int NPM = NP > 0 ? NP : CPFIT_MAXN;
-  constexpr int U = NP > 0 ? (LPE < 4 ? LPE : 4) : 1;
+  constexpr int U = NP > 0 ? (LPE < CPFIT_MTTKRP_U ? LPE : CPFIT_MTTKRP_U) : 1;
   const int np = NP > 0 ? NP : p.np;
   const int lane = threadIdx.x & 31;
   const int g = lane / LPE, q = lane % LPE;

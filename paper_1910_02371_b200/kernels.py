@@ -24,7 +24,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .core import SparseTensor, _dtype_code, cuda_device, current_stream
+from .core import SparseTensor, _dtype_code, cuda_device, current_stream, to_host
 from .exceptions import NumericalError
 from .validation import _is_torch, check_factor, check_factor_list, check_mode
 
@@ -93,7 +93,7 @@ def mttkrp(t: SparseTensor, factors, mode: int, threads: int = 1):
         _lib.check(_lib.load().cpfit_mttkrp(
             t.device_pattern().handle, mode, _dtype_code(dtype), rank, _vp(vals), 1,
             _ptrs(dev), _vp(out), _stream()), "mttkrp")
-    return out if on_device else out.cpu().numpy()
+    return out if on_device else to_host(out)
 
 
 def _tttp_slices(rank: int, h_slices, nnz: int, budget_bytes: int):
@@ -165,7 +165,7 @@ def gram_blocks(weights: SparseTensor, factors, mode: int, row_batches: int = 1,
         _lib.check(_lib.load().cpfit_gram(
             weights.device_pattern().handle, mode, _dtype_code(dtype), rank, _vp(w), 1,
             _ptrs(dev), _vp(gram), _stream()), "gram")
-    return gram if on_device else gram.cpu().numpy()
+    return gram if on_device else to_host(gram)
 
 
 def solve_factor(weights: SparseTensor, factors, rhs, mode: int, reg: float = 0.0,
@@ -212,8 +212,8 @@ def solve_factor(weights: SparseTensor, factors, rhs, mode: int, reg: float = 0.
                              f"(reg={reg})")
     _lib.check(st, "solve_factor")
     if not on_device:
-        x = x.cpu().numpy()
-        gram = gram.cpu().numpy() if gram is not None else None
+        x = to_host(x)
+        gram = to_host(gram) if gram is not None else None
     if return_gram:
         return x, gram
     return x
