@@ -6,9 +6,10 @@
 //   num_i = sum_{e in row i} rho_e partial_e, den_i = sum partial_e^2
 //   new_i = num_i / (den_i + reg) if den_i + reg > 0 else col_mode[i]
 //   resid_e = rho_e - partial_e * new[i(e)]
-// Pass A walks the mode-sorted tasks (warp per task, no atomics; split rows
-// combined in task order) and finalises new_i; pass B updates the residual
-// in canonical order (coalesced).  rho and resid use explicitly rounded
+// Pass A walks the mode-sorted tasks (warp per task, no atomics); split rows
+// are combined in a fixed order.  Pass B (residual) runs in canonical order
+// (coalesced) for modes with a permutation; for mode 0 (identity order) it is
+// fused into pass A for rows owned by one task.  rho and resid use explicitly rounded
 // (non-contracted) operations so each element follows the reference's
 // rounding; only the per-row sums are reassociated.
 #include "common.cuh"
@@ -50,6 +51,23 @@ __global__ void ccd_init_newcol(const CcdParams p) {
     p.new_col[i] = p.reg > 0.0 ? 0.0 / p.reg : p.old_col[i];  // empty rows: num = den = 0
 }
 
+// Residual update of the sorted entries [b0, b1) of one row (pass B):
+// rho = resid + part * old, resid = rho - part * new (reference rounding).
+__device__ __forceinline__ void ccd_update_range(const CcdParams &p, int64_t b0, int64_t b1,
+                                                 double oc, double nc) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = b0 + lane; e < b1; e += 32) {
+    const double part = ccd_partial_sorted(p, e);
+    const int64_t ent = p.perm ? __ldg(p.perm + e) : e;
+    const double rho = __dadd_rn(p.resid[ent], __dmul_rn(part, oc));
+    p.resid[ent] = __dsub_rn(rho, __dmul_rn(part, nc));
+  }
+}
+
+// Pass A (+ B for rows owned by one task): warp per task of the coarse table.
+// A row that fits one task is finished here -- its new value is known after
+// the warp's reduction, so the residual of its entries is updated right away
+// while they are still L1/L2-hot; split rows leave (num, den) partials.
 __global__ void __launch_bounds__(256) ccd_rows_kernel(const CcdParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -71,34 +89,48 @@ __global__ void __launch_bounds__(256) ccd_rows_kernel(const CcdParams p) {
       num += __shfl_xor_sync(0xffffffffu, num, o);
       den += __shfl_xor_sync(0xffffffffu, den, o);
     }
-    if (lane == 0) {
-      const int slot = p.task_slot[t];
-      if (slot < 0) {
-        const double dr = den + p.reg;
-        p.new_col[row] = dr > 0.0 ? num / dr : oc;
-      } else {
-        p.slots[2 * (int64_t)slot] = num;
-        p.slots[2 * (int64_t)slot + 1] = den;
-      }
+    const int slot = p.task_slot[t];
+    if (slot < 0) {
+      const double dr = den + p.reg;
+      const double nc = dr > 0.0 ? num / dr : oc;
+      if (lane == 0) p.new_col[row] = nc;
+      // identity order (mode 0): the fused residual pass stays coalesced;
+      // through a permutation a separate canonical-order pass is cheaper
+      if (!p.perm) ccd_update_range(p, b0, b1, oc, nc);
+    } else if (lane == 0) {
+      p.slots[2 * (int64_t)slot] = num;
+      p.slots[2 * (int64_t)slot + 1] = den;
     }
   }
 }
 
+// Split rows: warp per row, slots summed lane-strided then by a fixed xor
+// tree (deterministic), new value finalised.
 __global__ void ccd_combine(const CcdParams p, const int32_t *__restrict__ split_row,
                             const int32_t *__restrict__ split_slot, int64_t nsplit) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nsplit;
-       s += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < nsplit; s += nwarps) {
     const int64_t row = split_row[s];
     double num = 0.0, den = 0.0;
-    for (int64_t k = split_slot[s]; k < split_slot[s + 1]; ++k) {
+    for (int64_t k = split_slot[s] + lane; k < split_slot[s + 1]; k += 32) {
       num += p.slots[2 * k];
       den += p.slots[2 * k + 1];
     }
-    const double dr = den + p.reg;
-    p.new_col[row] = dr > 0.0 ? num / dr : p.old_col[row];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      num += __shfl_xor_sync(0xffffffffu, num, o);
+      den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    if (lane == 0) {
+      const double dr = den + p.reg;
+      p.new_col[row] = dr > 0.0 ? num / dr : p.old_col[row];
+    }
   }
 }
 
+// Pass B in canonical order (modes with a permutation): coalesced.
 __global__ void ccd_resid_kernel(const CcdParams p) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < p.nnz;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -112,6 +144,17 @@ __global__ void ccd_resid_kernel(const CcdParams p) {
     const int32_t i = __ldg(p.coords[p.mode] + e);
     const double rho = __dadd_rn(p.resid[e], __dmul_rn(part, __ldg(p.old_col + i)));
     p.resid[e] = __dsub_rn(rho, __dmul_rn(part, __ldg(p.new_col + i)));
+  }
+}
+
+// Pass B for the tasks of split rows only, identity order (mode 0).
+__global__ void __launch_bounds__(256) ccd_split_resid_kernel(const CcdParams p) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < p.ntasks; t += nwarps) {
+    if (p.task_slot[t] < 0) continue;
+    const int64_t row = p.task_row[t];
+    ccd_update_range(p, p.task_begin[t], p.task_begin[t + 1], p.old_col[row], p.new_col[row]);
   }
 }
 
@@ -161,12 +204,18 @@ int cpfit_ccd_update(cpfit_pattern *pt, int mode, const double *const *cols,
   ccd_rows_kernel<<<(unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks)), 256, 0, s>>>(p);
   CPFIT_LAUNCH_CHECK("ccd_rows");
   if (L.nsplit > 0) {
-    ccd_combine<<<grid_for(L.nsplit, 128), 128, 0, s>>>(p, L.split_row, L.split_slot,
-                                                       L.nsplit);
+    ccd_combine<<<grid_for(L.nsplit * 32, 256), 256, 0, s>>>(p, L.split_row, L.split_slot,
+                                                            L.nsplit);
     CPFIT_LAUNCH_CHECK("ccd_combine");
   }
-  ccd_resid_kernel<<<grid_for(pt->nnz, 256, 4), 256, 0, s>>>(p);
-  CPFIT_LAUNCH_CHECK("ccd_resid");
+  if (p.perm) {
+    ccd_resid_kernel<<<grid_for(pt->nnz, 256, 4), 256, 0, s>>>(p);
+    CPFIT_LAUNCH_CHECK("ccd_resid");
+  } else if (L.nsplit > 0) {
+    ccd_split_resid_kernel<<<(unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks)), 256, 0,
+                             s>>>(p);
+    CPFIT_LAUNCH_CHECK("ccd_split_resid");
+  }
   return CPFIT_OK;
 }
 
