@@ -134,6 +134,19 @@ int cpfit_solve_factor(cpfit_pattern *p, int mode, int dtype, int rank,
                        double reg, void *x_out, void *gram_out,
                        int64_t *bad_row, void *stream);
 
+/* One least-squares ALS mode update with the right-hand side fused into the
+ * Gram pass: rhs_i = sum_{e in row i} vals[e] h_e (the MTTKRP of `vals`,
+ * same h_e as the Gram), then (G_i + reg I) x_i = rhs_i with
+ * cpfit_solve_factor's semantics and error order.  The factor rows are
+ * gathered once per entry instead of twice.  vals_sorted as in cpfit_mttkrp;
+ * gram_out / rhs_out nullable.  Replaces the pair kernels.mttkrp +
+ * kernels.solve_factor in the ALS sweep (optim.py:214-228). */
+int cpfit_als_update(cpfit_pattern *p, int mode, int dtype, int rank,
+                     const void *vals, int vals_sorted,
+                     const void *const *factors, double reg, void *x_out,
+                     void *gram_out, void *rhs_out, int64_t *bad_row,
+                     void *stream);
+
 /* TTTP with an affine epilogue: out[e] = alpha * m_e + beta * vals[e], with
  * m_e = sum_r prod_n factors[n][i_n(e), r].  alpha = 2, beta = -2 gives the
  * least-squares derivative tensor 2(m - t) (losses.py:41-48, model via

@@ -35,7 +35,7 @@ SYMBOLS = (
     "cpfit_tttp", "cpfit_mttkrp", "cpfit_gram", "cpfit_solve_factor",
     "cpfit_tttp_axpby", "cpfit_sample", "cpfit_pattern_parent_index", "cpfit_gather_values",
     "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_update", "cpfit_probe_gather",
-    "cpfit_solve_rows", "cpfit_dense_reduce", "cpfit_khatri_rao",
+    "cpfit_solve_rows", "cpfit_dense_reduce", "cpfit_khatri_rao", "cpfit_als_update",
 )
 
 _vp = ctypes.c_void_p
@@ -95,6 +95,8 @@ def load(path: str | None = None):
                              ctypes.POINTER(_i64), _vp],
         "cpfit_dense_reduce": [_int, _i64, _i64, _int, _vp, _vp, _int, _vp, _vp],
         "cpfit_khatri_rao": [_int, _i64, _i64, _int, _vp, _vp, _vp, _vp],
+        "cpfit_als_update": [_vp, _int, _int, _int, _vp, _int, _PP, ctypes.c_double, _vp, _vp,
+                             _vp, ctypes.POINTER(_i64), _vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -48,7 +48,13 @@ struct GramParams {
   const int32_t *task_slot;
   int64_t ntasks;
   T *gram;      // dims[mode] x R x R
-  T *partial;   // nslots x R x R
+  T *partial;   // nslots x pstride (R x R, then R rhs values when vals != null)
+  int64_t pstride;
+  // fused right-hand side (ALS): rhs_i = sum_{e in row i} vals_e h_e, i.e. the
+  // MTTKRP of the data computed from the same staged Hadamard rows
+  const T *vals;          // nullable: no rhs
+  const int32_t *vperm;   // non-null: vals in canonical order, gather by perm
+  T *rhs;                 // dims[mode] x R
 };
 
 constexpr int GRAM_WARPS = 4;
@@ -92,6 +98,11 @@ gram_kernel(const GramParams<T> p) {
     double acc[NT][2];
 #pragma unroll
     for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = 0.0;
+    double racc[KV][VEC];  // rhs columns (k*LPE+q)*VEC+v over this group's slots
+#pragma unroll
+    for (int k = 0; k < KV; ++k)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) racc[k][v] = 0.0;
 
     for (int64_t base = b0; base < b1; base += GRAM_CHUNK) {
       const int cnt = (int)(b1 - base < GRAM_CHUNK ? b1 - base : GRAM_CHUNK);
@@ -101,12 +112,14 @@ gram_kernel(const GramParams<T> p) {
 #pragma unroll
       for (int n = 0; n < NPM; ++n) my_idx[n] = (n < np && lane < cnt) ? __ldg(p.idx[n] + e) : 0;
       double my_sw = 0.0;  // padded slots stage zero rows
+      double my_v = 0.0;
       if (lane < cnt) {
         my_sw = 1.0;
         if (p.weights) {
           T w = p.wperm ? __ldg(p.weights + __ldg(p.wperm + e)) : __ldg(p.weights + e);
           my_sw = sqrt((double)w);
         }
+        if (p.vals) my_v = (double)(p.vperm ? __ldg(p.vals + __ldg(p.vperm + e)) : __ldg(p.vals + e));
       }
       // stage sqrt(w) * h rows: group g handles slot j = s*G + g
 #pragma unroll
@@ -136,6 +149,7 @@ gram_kernel(const GramParams<T> p) {
         for (int u = 0; u < U; ++u) {
           const int j = (s0 + u) * G + g;
           const double sw = __shfl_sync(0xffffffffu, my_sw, j);
+          const double tv = __shfl_sync(0xffffffffu, my_v, j);
 #pragma unroll
           for (int k = 0; k < KV; ++k) {
             const int col = (k * LPE + q) * VEC;
@@ -147,6 +161,7 @@ gram_kernel(const GramParams<T> p) {
               for (int n = 1; n < NPM; ++n)
                 if (n < np) prod *= (double)x[u][n][k][v];
               h[v] = prod * sw;
+              racc[k][v] = fma(tv, prod, racc[k][v]);
             }
             if (col < RP) {
               if constexpr (VEC == 2) {
@@ -178,7 +193,26 @@ gram_kernel(const GramParams<T> p) {
     // store G (tiles and their mirror images)
     const int slot = p.task_slot[t];
     T *dst = slot < 0 ? p.gram + (int64_t)p.task_row[t] * rank * rank
-                      : p.partial + (int64_t)slot * rank * rank;
+                      : p.partial + (int64_t)slot * p.pstride;
+    if (p.vals) {
+      // fold the G groups' rhs partials (fixed xor tree), group 0 stores
+#pragma unroll
+      for (int o = LPE; o < 32; o <<= 1)
+#pragma unroll
+        for (int k = 0; k < KV; ++k)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) racc[k][v] += __shfl_xor_sync(0xffffffffu, racc[k][v], o);
+      T *rdst = slot < 0 ? p.rhs + (int64_t)p.task_row[t] * rank : dst + rank * rank;
+      if (g == 0) {
+#pragma unroll
+        for (int k = 0; k < KV; ++k)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            const int col = (k * LPE + q) * VEC + v;
+            if (col < rank) rdst[col] = (T)racc[k][v];
+          }
+      }
+    }
     if constexpr (RP <= GRAM_CHUNK) {
       // transpose through the staging buffer, then write whole rows coalesced
       int tile = 0;
@@ -224,15 +258,17 @@ gram_kernel(const GramParams<T> p) {
 template <typename T>
 __global__ void combine_gram_partials(const int32_t *__restrict__ split_row,
                                       const int32_t *__restrict__ split_slot, int64_t nsplit,
-                                      int64_t rr, const T *__restrict__ partial,
-                                      T *__restrict__ gram) {
+                                      int64_t rr, int64_t pstride,
+                                      const T *__restrict__ partial, T *__restrict__ gram,
+                                      T *__restrict__ rhs, int rank) {
   for (int64_t s = blockIdx.x; s < nsplit; s += gridDim.x) {
     const int64_t row = split_row[s];
     const int64_t a = split_slot[s], b = split_slot[s + 1];
-    for (int64_t c = threadIdx.x; c < rr; c += blockDim.x) {
-      double acc = (double)partial[a * rr + c];
-      for (int64_t k = a + 1; k < b; ++k) acc += (double)partial[k * rr + c];
-      gram[row * rr + c] = (T)acc;
+    for (int64_t c = threadIdx.x; c < pstride; c += blockDim.x) {
+      double acc = (double)partial[a * pstride + c];
+      for (int64_t k = a + 1; k < b; ++k) acc += (double)partial[k * pstride + c];
+      if (c < rr) gram[row * rr + c] = (T)acc;
+      else rhs[row * rank + (c - rr)] = (T)acc;
     }
   }
 }
@@ -305,7 +341,8 @@ static int launch_gram(const GramParams<T> &p, cudaStream_t s) {
 // empty slices).  Weights: nullptr = unit mask.
 template <typename T>
 static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
-                    int weights_sorted, const void *const *factors, T *gram, cudaStream_t s) {
+                    int weights_sorted, const void *const *factors, T *gram, cudaStream_t s,
+                    const T *vals = nullptr, int vals_sorted = 0, T *rhs = nullptr) {
   const int64_t dim = pt->dims[mode];
   const int64_t rr = (int64_t)rank * rank;
   if (weights && pt->nnz > 0) {
@@ -323,6 +360,7 @@ static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
     }
   }
   CPFIT_CUDA(cudaMemsetAsync(gram, 0, (size_t)dim * rr * sizeof(T), s));
+  if (vals) CPFIT_CUDA(cudaMemsetAsync(rhs, 0, (size_t)dim * rank * sizeof(T), s));
   if (pt->nnz == 0) return CPFIT_OK;
   CPFIT_TRY(ensure_coarse_layout(pt, mode, s));
   CpfitModeLayout &L = pt->coarse[mode];
@@ -351,14 +389,18 @@ static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
   p.task_slot = L.task_slot;
   p.ntasks = L.ntasks;
   p.gram = gram;
+  p.vals = vals;
+  p.vperm = (vals && !vals_sorted) ? L.perm : nullptr;
+  p.rhs = rhs;
+  p.pstride = rr + (vals ? rank : 0);
   Scratch<T> partial(s);
-  if (L.nslots > 0) CPFIT_TRY(partial.alloc((size_t)L.nslots * rr));
+  if (L.nslots > 0) CPFIT_TRY(partial.alloc((size_t)L.nslots * p.pstride));
   p.partial = partial.ptr;
   CPFIT_TRY(launch_gram<T>(p, s));
   if (L.nsplit > 0) {
     unsigned grid = (unsigned)(L.nsplit < 65535 ? L.nsplit : 65535);
     combine_gram_partials<T><<<grid, 256, 0, s>>>(L.split_row, L.split_slot, L.nsplit, rr,
-                                                  partial.ptr, gram);
+                                                  p.pstride, partial.ptr, gram, rhs, rank);
     CPFIT_LAUNCH_CHECK("combine_gram_partials");
   }
   return CPFIT_OK;
@@ -826,6 +868,35 @@ static int run_solve_factor(cpfit_pattern *pt, int mode, int rank, const void *w
                       bad_row ? bad_row : &dummy, s);
 }
 
+// One ALS mode update (optim.py:214-228 with kernels.py:222-265): the
+// right-hand side (MTTKRP of the data) is accumulated by the Gram kernel from
+// the same staged Hadamard rows, so the factor rows are gathered once.
+template <typename T>
+static int run_als_update(cpfit_pattern *pt, int mode, int rank, const void *vals,
+                          int vals_sorted, const void *const *factors, double reg, void *x_out,
+                          void *gram_out, void *rhs_out, int64_t *bad_row, cudaStream_t s) {
+  const int64_t dim = pt->dims[mode];
+  Scratch<T> gtmp(s), rtmp(s);
+  T *gram = (T *)gram_out, *rhs = (T *)rhs_out;
+  if (!gram) {
+    CPFIT_TRY(gtmp.alloc((size_t)dim * rank * rank));
+    gram = gtmp.ptr;
+  }
+  if (!rhs) {
+    CPFIT_TRY(rtmp.alloc((size_t)dim * rank));
+    rhs = rtmp.ptr;
+  }
+  CPFIT_TRY(run_gram<T>(pt, mode, rank, nullptr, 0, factors, gram, s, (const T *)vals,
+                        vals_sorted, rhs));
+  if (reg < 0.0) {
+    set_error("regularization must be >= 0");
+    return CPFIT_EINVAL;
+  }
+  CPFIT_TRY(ensure_layout(pt, mode, s));
+  int64_t dummy = -1;
+  return run_solve<T>(pt, mode, rank, gram, rhs, reg, (T *)x_out, bad_row ? bad_row : &dummy, s);
+}
+
 }  // namespace cpfit
 
 using namespace cpfit;
@@ -891,6 +962,26 @@ int cpfit_solve_factor(cpfit_pattern *p, int mode, int dtype, int rank, const vo
   if (dtype == CPFIT_F32)
     return run_solve_factor<float>(p, mode, rank, weights, weights_sorted, factors, rhs, reg,
                                    x_out, gram_out, bad_row, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+int cpfit_als_update(cpfit_pattern *p, int mode, int dtype, int rank, const void *vals,
+                     int vals_sorted, const void *const *factors, double reg, void *x_out,
+                     void *gram_out, void *rhs_out, int64_t *bad_row, void *stream) {
+  if (!p || mode < 0 || mode >= p->order) {
+    set_error("mode %d out of range for order-%d tensor", mode, p ? p->order : 0);
+    return CPFIT_EINVAL;
+  }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  if (!vals && p->nnz > 0) { set_error("values are required"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64)
+    return run_als_update<double>(p, mode, rank, vals, vals_sorted, factors, reg, x_out,
+                                  gram_out, rhs_out, bad_row, s);
+  if (dtype == CPFIT_F32)
+    return run_als_update<float>(p, mode, rank, vals, vals_sorted, factors, reg, x_out,
+                                 gram_out, rhs_out, bad_row, s);
   set_error("unknown dtype %d", dtype);
   return CPFIT_EINVAL;
 }

@@ -210,9 +210,9 @@ def _stream():
 
 def _als_mode_device(t: SparseTensor, F, mode: int, reg: float, keep_gram: bool = False,
                      row_offset: int = 0):
-    """One least-squares ALS mode update on the device: rhs = MTTKRP of the
-    data, then the fused Gram assembly (unit weights: the observation mask is
-    never materialised) + batched SPD solve.  Returns x (or (x, gram, rhs))
+    """One least-squares ALS mode update on the device: the Gram assembly
+    with the MTTKRP right-hand side fused in (unit weights: the observation
+    mask is never materialised) + batched SPD solve.  Returns x (or (x, gram, rhs))
     with t.shape[mode] rows; F[mode] is not read (t's mode may be a rebased
     row block of a larger factor -- dist.ShardedALS)."""
     torch = _torch()
@@ -224,23 +224,19 @@ def _als_mode_device(t: SparseTensor, F, mode: int, reg: float, keep_gram: bool 
     pat = t.device_pattern()
     ptrs = _ptrs([None if n == mode else f for n, f in enumerate(F)])
     rhs = torch.empty((t.shape[mode], rank), dtype=dtype, device=dev)
-    if t.nnz:
-        vals = t.sorted_values(mode, dtype)
-        _lib.check(L.cpfit_mttkrp(pat.handle, mode, code, rank,
-                                  ctypes.c_void_p(vals.data_ptr()), 1, ptrs,
-                                  ctypes.c_void_p(rhs.data_ptr()), _stream()), "mttkrp")
-    else:
-        rhs.zero_()
+    vals = t.sorted_values(mode, dtype) if t.nnz else None
     x = torch.empty_like(rhs)
     # always a torch-cached buffer: a library-side scratch of I_n x R x R would
     # hit the stream-ordered pool's allocate/release path on every call
     gram = torch.empty((t.shape[mode], rank, rank), dtype=dtype, device=dev)
     bad = ctypes.c_int64(-1)
-    st = L.cpfit_solve_factor(pat.handle, mode, code, rank, None, 1, ptrs,
-                              ctypes.c_void_p(rhs.data_ptr()), float(reg),
-                              ctypes.c_void_p(x.data_ptr()),
-                              ctypes.c_void_p(gram.data_ptr()),
-                              ctypes.byref(bad), _stream())
+    # rhs (MTTKRP of the data) accumulated by the Gram pass itself: one gather
+    # of the factor rows per entry (cpfit_als_update)
+    st = L.cpfit_als_update(pat.handle, mode, code, rank,
+                            None if vals is None else ctypes.c_void_p(vals.data_ptr()), 1, ptrs,
+                            float(reg), ctypes.c_void_p(x.data_ptr()),
+                            ctypes.c_void_p(gram.data_ptr()), ctypes.c_void_p(rhs.data_ptr()),
+                            ctypes.byref(bad), _stream())
     if st == _lib.EEMPTYROW:
         raise NumericalError(
             f"alternating solve failed: mode {mode} row {bad.value + row_offset}: no incident "
@@ -249,7 +245,7 @@ def _als_mode_device(t: SparseTensor, F, mode: int, reg: float, keep_gram: bool 
         raise NumericalError(f"alternating solve failed: mode {mode} row "
                              f"{bad.value + row_offset}: singular normal equations "
                              f"(reg={float(reg)})")
-    _lib.check(st, "solve_factor")
+    _lib.check(st, "als_update")
     if keep_gram:
         return x, gram, rhs
     return x

@@ -311,3 +311,37 @@ def test_gram_symmetric_psd():
     for i in range(5):
         np.linalg.cholesky(g[i] + 1e-8 * np.eye(3))
         assert np.allclose(g[i], g[i].T, atol=1e-12)
+
+
+@pytest.mark.parametrize("rank", [3, 16, 24, 64])
+def test_fused_als_update_vs_oracle(rank):
+    """cpfit_als_update: the Gram pass also accumulates the MTTKRP right-hand
+    side; gram, rhs and x must match the oracle's separate mttkrp / gram /
+    solve (kernels.py:46-91, 190-265), including split (Zipf-head) rows."""
+    torch = _torch()
+    import ctypes
+
+    from paper_1910_02371_b200.optim import _als_mode_device
+    rng = np.random.default_rng(rank)
+    dims = (40, 300, 200)
+    n = 40000
+    i0 = synth.zipf_indices(rng, dims[0], n)
+    i1 = rng.integers(0, dims[1], n)
+    i2 = rng.integers(0, dims[2], n)
+    t = cp.from_coords([i0, i1, i2], rng.standard_normal(n), dims)
+    ot = O.OTensor(dims, t.keys, t.values)
+    fs = [rng.random((d, rank)) for d in dims]
+    omask = ot.with_values(np.ones(ot.nnz))
+    for task in (64, 1024):
+        t.set_task_size(task)
+        for mode in range(3):
+            F = [torch.from_numpy(f).cuda() for f in fs]
+            x, gram, rhs = _als_mode_device(t, F, mode, 1e-3, keep_gram=True)
+            orhs = O.mttkrp(ot, fs, mode)
+            assert rel(rhs.cpu().numpy(), orhs) < 1e-12
+            assert rel(gram.cpu().numpy(), O.gram_blocks(omask, fs, mode)) < 1e-12
+            ox = O.solve_factor(omask, fs, orhs, mode, 1e-3)
+            assert rel(x.cpu().numpy(), ox) < 1e-9
+            # run-to-run bitwise
+            x2 = _als_mode_device(t, F, mode, 1e-3)
+            assert torch.equal(x, x2)
