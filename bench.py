@@ -57,7 +57,7 @@ def peaks():
 
 
 # ---------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (NVML / nvidia-smi during the timed region)
 
 REASON_BITS = {
     0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -68,15 +68,32 @@ REASON_BITS = {
 
 
 class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region.  NVML
+    (nvidia-ml-py) polled from a thread every ~2 ms, so even a 40 ms region
+    gets many samples; ``nvidia-smi -lms 50`` if NVML is unavailable."""
+
     def __init__(self, index: int = 0):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.nvml = None
+        self.lines = []  # (time, sm_mhz, max_mhz, reasons)
         self.marks = []
+        self._stop = threading.Event()
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (pynvml, h)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         cmd = ["nvidia-smi", f"--id={self.index}",
-               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu",
+               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                "--format=csv,noheader,nounits", "-lms", "50"]
         try:
             self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
@@ -84,47 +101,59 @@ class ClockSampler:
         except Exception:
             self.proc = None
             return
-        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t = threading.Thread(target=self._read_smi, daemon=True)
         self.t.start()
+        t_end = time.perf_counter() + 10.0
+        while not self.lines and time.perf_counter() < t_end and self.proc.poll() is None:
+            time.sleep(0.02)
 
-    def _read(self):
+    def _poll_nvml(self):
+        pynvml, h = self.nvml
+        while not self._stop.is_set():
+            try:
+                sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                r = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+            except Exception:
+                return
+            self.lines.append((time.perf_counter(), sm, self.max_mhz, r))
+            time.sleep(0.002)
+
+    def _read_smi(self):
         for line in self.proc.stdout:
-            self.lines.append((time.perf_counter(), line.strip()))
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                r = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
+                self.lines.append((time.perf_counter(), float(parts[0]), float(parts[1]), r))
+            except (ValueError, IndexError):
+                continue
 
     def mark(self, tag):
         self.marks.append((tag, time.perf_counter()))
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        self._stop.set()
+        if self.proc is None and self.nvml is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
         t0 = dict(self.marks).get("start", 0.0)
         t1 = dict(self.marks).get("stop", time.perf_counter())
-        sm, mx, reasons, util = [], [], 0, []
-        window = [l for (t, l) in self.lines if t0 - 0.06 <= t <= t1 + 0.06] or \
-            [l for (_, l) in self.lines]
-        for l in window:
-            parts = [p.strip() for p in l.split(",")]
-            if len(parts) < 4:
-                continue
-            try:
-                s, m = float(parts[0]), float(parts[1])
-                r = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
-                u = float(parts[3])
-            except ValueError:
-                continue
-            sm.append(s)
-            mx.append(m)
-            util.append(u)
-            reasons |= r
-        names = [n for b, n in REASON_BITS.items() if reasons & b and n != "gpu_idle"]
+        window = [x for x in self.lines if t0 <= x[0] <= t1]
+        if not window:  # region shorter than the sampling period: nearest samples
+            window = sorted(self.lines, key=lambda x: abs(x[0] - 0.5 * (t0 + t1)))[:2]
+        reasons = 0
+        for x in window:
+            reasons |= x[3]
+        names = [n for bit, n in REASON_BITS.items() if reasons & bit and n != "gpu_idle"]
+        sm = [x[1] for x in window]
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": names, "samples": len(sm)}
+                "sm_max_mhz": max(x[2] for x in window) if window else None,
+                "reasons": names, "samples": len(sm),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
@@ -289,7 +318,7 @@ def als_section(world, rank, dev, sweeps=3):
         coords = coords[::-1]
         del rem
         als = D.ShardedALS(coords, vals, shape, REG, D.DeviceBackend())
-        del coords, keys
+        del coords
         F = [f.clone() for f in init]
         als.sweep(F)
         torch.cuda.synchronize()
@@ -308,6 +337,22 @@ def als_section(world, rank, dev, sweeps=3):
             times.append(float(ms.item()))
         out["als_sweep_ms"] = float(np.mean(times))
         out["parallelism"] = f"row-sharded x{world}, NCCL all-gather of factor rows per mode"
+        del als
+        torch.cuda.empty_cache()
+        # CCD++: nonzero-sharded, one all-reduce of (num, den) per (r, mode)
+        ccd = D.ShardedCCD(keys, vals, shape, REG, D.DeviceBackend())
+        F = [f.clone() for f in init]
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ccd.sweep(F)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        out["ccd_sweep_ms"] = float(ms.item())
+        out["ccd_parallelism"] = f"nnz-sharded x{world}, NCCL all-reduce of (num, den)"
     out["als_sweep_cpu_reference_s"] = CPU_ALS_SURVEY_S
     out["als_speedup_vs_cpu_reference"] = CPU_ALS_SURVEY_S * 1e3 / out["als_sweep_ms"]
     out["cpu_reference_note"] = ("reference cpfit (numba + OpenBLAS, 8 vCPU Xeon) measured in "
@@ -319,7 +364,7 @@ CPU_DENSE_EINSUM_S = [1.80, 0.44, 0.47]  # host numpy.einsum per mode, 8 vCPU (S
 CPU_CFG5_SCALED = {"tttp_s_at_1e7": 3.56, "sgd_step_s_at_1e7": 1.11}  # SURVEY.md 6, f64 numpy
 
 
-def sgd_section(dev, steps=5):
+def sgd_section(dev, steps=5, world=1):
     """BASELINE cfg 5 on one GPU: order-4 fp32 tensor 1e5^3 x 1e3 with 1e9
     distinct uniform nonzeros (device-generated, values = rank-8 CP model +
     N(0, 0.1) via the library's TTTP), R=64: SGD steps (1% Bernoulli sample,
@@ -331,22 +376,43 @@ def sgd_section(dev, steps=5):
     from paper_1910_02371_b200.losses import sum_sq, tttp_affine
     from paper_1910_02371_b200.optim import SolverConfig, _sgd_ls_device
     t0 = time.perf_counter()
-    shape, tn, values, F = synth.cfg5_device()
+    shape, tn, values, F, keys = synth.cfg5_device(with_keys=True)
     t = tn.with_values(values)
     gen_s = time.perf_counter() - t0
     cfg = SolverConfig(rank=64, algorithm="sgd", step=1e-3, reg=1e-4, sample_rate=0.01)
     stream = torch.cuda.current_stream()
     root = cp.RngState(5).child(1)
-    _sgd_ls_device(t, F, cfg, root.child(0))  # warm-up
+    if world > 1:
+        # nonzero shards, global Philox counter, one all-reduce per mode
+        import torch.distributed as dist
+
+        from paper_1910_02371_b200 import dist as D
+        sharded = D.ShardedSGD(keys, values, shape, D.DeviceBackend())
+
+        def one(rng):
+            sharded.step(F, cfg.sample_rate, cfg.step, cfg.reg, rng)
+            return None
+    else:
+        def one(rng):
+            return _sgd_ls_device(t, F, cfg, rng)
+    del keys
+    one(root.child(0))  # warm-up
     torch.cuda.synchronize()
     ms, kept = [], []
     for it in range(1, steps + 1):
+        if world > 1:
+            dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        kept.append(_sgd_ls_device(t, F, cfg, root.child(it)))
+        kept.append(one(root.child(it)))
         b.record(stream)
         torch.cuda.synchronize()
-        ms.append(a.elapsed_time(b))
+        m = a.elapsed_time(b)
+        if world > 1:
+            mt = torch.tensor([m], dtype=torch.float64, device=dev)
+            dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+            m = float(mt.item())
+        ms.append(m)
     resid = tttp_affine(t, F, -1.0, 1.0, torch.float32)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -359,8 +425,8 @@ def sgd_section(dev, steps=5):
     alg = t.nnz * (4 * 4 + 2 * 4 + 4 * 64 * 4)  # 1,048 B per nnz
     return {"workload": "BASELINE cfg 5: order 4, 1e5x1e5x1e5x1e3, 1e9 uniform distinct nnz, "
                         "fp32, R=64; SGD rate 0.01 (Bernoulli), step 1e-3, lambda 1e-4",
-            "generation_s": gen_s, "nnz": t.nnz,
-            "sgd_step_ms": float(np.mean(ms)), "sample_nnz_per_step": float(np.mean(kept)),
+            "generation_s": gen_s, "nnz": t.nnz, "n_gpus": world,
+            "sgd_step_ms": float(np.mean(ms)), "sample_nnz_per_step": (float(np.mean(kept)) if world == 1 else None),
             "tttp_residual_ms": tttp_ms,
             "tttp_residual_nnz_per_s": t.nnz / (tttp_ms * 1e-3),
             "tttp_residual_alg_gbs": alg / (tttp_ms * 1e-3) / 1e9,
@@ -643,10 +709,10 @@ def main():
         except Exception as exc:
             dense = {"error": repr(exc)}
     sgd = None
-    if not args.no_sgd and world == 1:
+    if not args.no_sgd:
         torch.cuda.empty_cache()
         try:
-            sgd = sgd_section(dev)
+            sgd = sgd_section(dev, world=world)
         except Exception as exc:
             sgd = {"error": repr(exc)}
         torch.cuda.empty_cache()

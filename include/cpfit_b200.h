@@ -195,6 +195,21 @@ int cpfit_ccd_update(cpfit_pattern *p, int mode, const double *const *cols,
                      const double *old_col, double *new_col, double *resid,
                      double reg, void *stream);
 
+/* Distributed CCD++ (nonzeros sharded, one all-reduce per
+ * (r, mode)).  cpfit_ccd_numden writes this shard's per-row sums
+ * numden[i] = sum rho_e partial_e, numden[I_n + i] = sum partial_e^2
+ * (2 * dims[mode] doubles, zero for rows without local entries);
+ * after the caller sums numden over ranks, cpfit_ccd_apply computes
+ * new_col[i] = num / (den + reg) (old_col[i] when den + reg <= 0) and
+ * updates the residual of the local entries.  On one rank the pair equals
+ * cpfit_ccd_update bit for bit. */
+int cpfit_ccd_numden(cpfit_pattern *p, int mode, const double *const *cols,
+                     const double *old_col, const double *resid, double *numden,
+                     void *stream);
+int cpfit_ccd_apply(cpfit_pattern *p, int mode, const double *const *cols,
+                    const double *old_col, const double *numden, double reg,
+                    double *new_col, double *resid, void *stream);
+
 /* Batched regularised SPD solves without a tensor pattern:
  * (G_i + reg I) x_i = rhs_i for i < nrows, G_i = gram + i * gram_stride
  * (gram_stride 0: one shared G, e.g. the dense CP-ALS Gram (B^T B)*(C^T C)).

@@ -32,6 +32,7 @@ struct CcdParams {
   double *slots;          // 2 * nslots (num, den)
   double *resid;
   double reg;
+  double *numden;         // non-null: emit (num, den) per row, [num(I_n), den(I_n)], and stop
 };
 
 __device__ __forceinline__ double ccd_partial_sorted(const CcdParams &p, int64_t e) {
@@ -90,7 +91,12 @@ __global__ void __launch_bounds__(256) ccd_rows_kernel(const CcdParams p) {
       den += __shfl_xor_sync(0xffffffffu, den, o);
     }
     const int slot = p.task_slot[t];
-    if (slot < 0) {
+    if (slot < 0 && p.numden) {
+      if (lane == 0) {
+        p.numden[row] = num;
+        p.numden[p.dim + row] = den;
+      }
+    } else if (slot < 0) {
       const double dr = den + p.reg;
       const double nc = dr > 0.0 ? num / dr : oc;
       if (lane == 0) p.new_col[row] = nc;
@@ -123,10 +129,22 @@ __global__ void ccd_combine(const CcdParams p, const int32_t *__restrict__ split
       num += __shfl_xor_sync(0xffffffffu, num, o);
       den += __shfl_xor_sync(0xffffffffu, den, o);
     }
-    if (lane == 0) {
+    if (lane == 0 && p.numden) {
+      p.numden[row] = num;
+      p.numden[p.dim + row] = den;
+    } else if (lane == 0) {
       const double dr = den + p.reg;
       p.new_col[row] = dr > 0.0 ? num / dr : p.old_col[row];
     }
+  }
+}
+
+// Distributed CCD++: new value from the all-reduced (num, den) of every row.
+__global__ void ccd_finalize_kernel(const CcdParams p) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.dim;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double dr = p.numden[p.dim + i] + p.reg;
+    p.new_col[i] = dr > 0.0 ? p.numden[i] / dr : p.old_col[i];
   }
 }
 
@@ -162,19 +180,24 @@ __global__ void __launch_bounds__(256) ccd_split_resid_kernel(const CcdParams p)
 
 using namespace cpfit;
 
+static unsigned ccd_task_grid(int64_t ntasks) {
+  int64_t blocks = (ntasks + 7) / 8;
+  int64_t cap = (int64_t)num_sms() * 8;
+  return (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
 extern "C" {
 
-int cpfit_ccd_update(cpfit_pattern *pt, int mode, const double *const *cols,
+static int ccd_setup(cpfit_pattern *pt, int mode, const double *const *cols,
                      const double *old_col, double *new_col, double *resid, double reg,
-                     void *stream) {
+                     cudaStream_t s, CcdParams &p) {
   if (!pt || mode < 0 || mode >= pt->order) {
     set_error("mode %d out of range", mode);
     return CPFIT_EINVAL;
   }
-  cudaStream_t s = (cudaStream_t)stream;
   CPFIT_TRY(ensure_layout(pt, mode, s));
   CpfitModeLayout &L = pt->modes[mode];
-  CcdParams p{};
+  p = CcdParams{};
   p.order = pt->order;
   p.mode = mode;
   p.nnz = pt->nnz;
@@ -193,29 +216,77 @@ int cpfit_ccd_update(cpfit_pattern *pt, int mode, const double *const *cols,
   p.new_col = new_col;
   p.resid = resid;
   p.reg = reg;
+  return CPFIT_OK;
+}
+
+// pass A (+ split-row combine): finalises new_col, or fills p.numden
+static int ccd_pass_a(cpfit_pattern *pt, CcdParams &p, cudaStream_t s) {
+  CpfitModeLayout &L = pt->modes[p.mode];
   Scratch<double> slots(s);
   if (L.nslots > 0) CPFIT_TRY(slots.alloc(2 * L.nslots));
   p.slots = slots.ptr;
-  ccd_init_newcol<<<grid_for(p.dim, 256), 256, 0, s>>>(p);
-  CPFIT_LAUNCH_CHECK("ccd_init_newcol");
+  if (p.numden) {
+    CPFIT_CUDA(cudaMemsetAsync(p.numden, 0, 2 * (size_t)p.dim * sizeof(double), s));
+  } else {
+    ccd_init_newcol<<<grid_for(p.dim, 256), 256, 0, s>>>(p);
+    CPFIT_LAUNCH_CHECK("ccd_init_newcol");
+  }
   if (pt->nnz == 0) return CPFIT_OK;
-  int64_t blocks = (L.ntasks + 7) / 8;
-  int64_t cap = (int64_t)num_sms() * 8;
-  ccd_rows_kernel<<<(unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks)), 256, 0, s>>>(p);
+  ccd_rows_kernel<<<ccd_task_grid(L.ntasks), 256, 0, s>>>(p);
   CPFIT_LAUNCH_CHECK("ccd_rows");
   if (L.nsplit > 0) {
     ccd_combine<<<grid_for(L.nsplit * 32, 256), 256, 0, s>>>(p, L.split_row, L.split_slot,
                                                             L.nsplit);
     CPFIT_LAUNCH_CHECK("ccd_combine");
   }
+  return CPFIT_OK;
+}
+
+int cpfit_ccd_update(cpfit_pattern *pt, int mode, const double *const *cols,
+                     const double *old_col, double *new_col, double *resid, double reg,
+                     void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  CcdParams p;
+  CPFIT_TRY(ccd_setup(pt, mode, cols, old_col, new_col, resid, reg, s, p));
+  CPFIT_TRY(ccd_pass_a(pt, p, s));
+  if (pt->nnz == 0) return CPFIT_OK;
+  CpfitModeLayout &L = pt->modes[mode];
   if (p.perm) {
     ccd_resid_kernel<<<grid_for(pt->nnz, 256, 4), 256, 0, s>>>(p);
     CPFIT_LAUNCH_CHECK("ccd_resid");
   } else if (L.nsplit > 0) {
-    ccd_split_resid_kernel<<<(unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks)), 256, 0,
-                             s>>>(p);
+    ccd_split_resid_kernel<<<ccd_task_grid(L.ntasks), 256, 0, s>>>(p);
     CPFIT_LAUNCH_CHECK("ccd_split_resid");
   }
+  return CPFIT_OK;
+}
+
+int cpfit_ccd_numden(cpfit_pattern *pt, int mode, const double *const *cols,
+                     const double *old_col, const double *resid, double *numden,
+                     void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  CcdParams p;
+  CPFIT_TRY(ccd_setup(pt, mode, cols, old_col, nullptr, const_cast<double *>(resid), 0.0, s, p));
+  if (!numden) {
+    set_error("numden is required");
+    return CPFIT_EINVAL;
+  }
+  p.numden = numden;
+  return ccd_pass_a(pt, p, s);
+}
+
+int cpfit_ccd_apply(cpfit_pattern *pt, int mode, const double *const *cols,
+                    const double *old_col, const double *numden, double reg, double *new_col,
+                    double *resid, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  CcdParams p;
+  CPFIT_TRY(ccd_setup(pt, mode, cols, old_col, new_col, resid, reg, s, p));
+  p.numden = const_cast<double *>(numden);
+  ccd_finalize_kernel<<<grid_for(p.dim, 256), 256, 0, s>>>(p);
+  CPFIT_LAUNCH_CHECK("ccd_finalize");
+  if (pt->nnz == 0) return CPFIT_OK;
+  ccd_resid_kernel<<<grid_for(pt->nnz, 256, 4), 256, 0, s>>>(p);
+  CPFIT_LAUNCH_CHECK("ccd_resid");
   return CPFIT_OK;
 }
 

@@ -13,7 +13,9 @@ NVLink/NVSwitch).  No other exchange: factors are replicated.
 SGD shards *nonzeros* (contiguous key ranges); the device Philox sampler uses
 the global entry index as its counter, so the union of the shard samples is
 the single-device sample bit for bit, and the per-mode gradients are summed
-with one all-reduce.
+with one all-reduce (``ShardedSGD``).  CCD++ shards nonzeros too and
+all-reduces the per-row (num, den) sums of every (r, mode) column update
+(``ShardedCCD``).
 
 The partition / shard / assembly logic is backend-neutral: ``LocalBackend``
 objects supply the row-local compute.  ``DeviceBackend`` runs the CUDA
@@ -132,6 +134,76 @@ class ShardedALS:
         return factors
 
 
+class ShardedCCD:
+    """Nonzero-sharded CCD++ sweeps: each rank keeps a
+    contiguous key range of the entries and its slice of the residual; per
+    (r, mode) the per-row (num, den) sums of the shard are all-reduced (2 I_n
+    values) and every rank computes the identical new column, then updates
+    its local residual.  optim.py:235-268 least-squares branch.
+
+    backend: ccd_begin(shard, factors) -> state; ccd_numden(shard, state, r,
+    mode) -> comm tensor (2 I_n); ccd_apply(shard, state, r, mode, numden, reg);
+    ccd_end(state, factors); make_nnz_shard(shape, keys, values)."""
+
+    def __init__(self, keys, values, shape, reg, backend, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.shape = tuple(shape)
+        self.reg = float(reg)
+        self.backend = backend
+        self.lo, self.hi = nnz_partition(len(keys), self.world)[self.rank]
+        self.shard = backend.make_nnz_shard(self.shape, keys[self.lo:self.hi],
+                                            values[self.lo:self.hi])
+
+    def sweep(self, factors):
+        b = self.backend
+        state = b.ccd_begin(self.shard, factors)
+        rank = factors[0].shape[1]
+        for r in range(rank):
+            for mode in range(len(self.shape)):
+                nd = b.ccd_numden(self.shard, state, r, mode)
+                if self.world > 1:
+                    self.dist.all_reduce(nd, group=self.group)
+                b.ccd_apply(self.shard, state, r, mode, nd, self.reg)
+        b.ccd_end(state, factors)
+        return factors
+
+
+class ShardedSGD:
+    """Nonzero-sharded SGD steps: rank p samples its key range
+    with the global Philox counter (the union of the shard samples is the
+    single-device sample bit for bit), computes the least-squares gradient
+    MTTKRPs of its sample, the gradients are summed with one all-reduce per
+    mode and every rank applies the identical update (optim.py:300-330).
+
+    backend: make_nnz_shard; sgd_grads(shard, factors, rate, rng, counter_offset)
+    -> list of comm tensors; sgd_apply(factors, grads, step, shrink)."""
+
+    def __init__(self, keys, values, shape, backend, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.shape = tuple(shape)
+        self.backend = backend
+        self.lo, self.hi = nnz_partition(len(keys), self.world)[self.rank]
+        self.shard = backend.make_nnz_shard(self.shape, keys[self.lo:self.hi],
+                                            values[self.lo:self.hi])
+
+    def step(self, factors, rate: float, step: float, reg: float, rng):
+        b = self.backend
+        grads = b.sgd_grads(self.shard, factors, rate, rng, self.lo)
+        if self.world > 1:
+            for g in grads:
+                self.dist.all_reduce(g, group=self.group)
+        b.sgd_apply(factors, grads, step, 2.0 * step * reg * rate)
+        return factors
+
+
 class DeviceBackend:
     """CUDA kernels + NCCL (factors are CUDA tensors)."""
 
@@ -149,6 +221,70 @@ class DeviceBackend:
         with the shard's own (rebased) mode factor slot unused."""
         from .optim import _als_mode_device
         return _als_mode_device(shard, factors, mode, reg, row_offset=lo)
+
+    def make_nnz_shard(self, shape, keys, values):
+        from .core import SparseTensor
+        return SparseTensor.from_device(shape, keys.contiguous(), values.contiguous())
+
+    # -- CCD++ (cpfit_ccd_numden / cpfit_ccd_apply) --
+    def ccd_begin(self, shard, factors):
+        torch = self.torch
+        from .losses import tttp_affine
+        cols = [f.t().contiguous() for f in factors]  # R x I_n
+        resid = tttp_affine(shard, factors, -1.0, 1.0, torch.float64)
+        tmp = [torch.empty(d, dtype=torch.float64, device=factors[0].device)
+               for d in shard.shape]
+        return {"cols": cols, "resid": resid, "tmp": tmp}
+
+    def _ccd_ptrs(self, state, r):
+        import ctypes
+
+        from . import _lib
+        cp = [c[r] for c in state["cols"]]
+        arr = _lib.ptr_array([c.data_ptr() for c in cp])
+        return cp, arr, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
+
+    def ccd_numden(self, shard, state, r, mode):
+        import ctypes
+
+        from . import _lib
+        from .optim import _stream
+        cp, _keep, ptrs = self._ccd_ptrs(state, r)
+        nd = self.torch.empty(2 * shard.shape[mode], dtype=self.torch.float64,
+                              device=cp[0].device)
+        _lib.check(_lib.load().cpfit_ccd_numden(
+            shard.device_pattern().handle, mode, ptrs, ctypes.c_void_p(cp[mode].data_ptr()),
+            ctypes.c_void_p(state["resid"].data_ptr()), ctypes.c_void_p(nd.data_ptr()),
+            _stream()), "ccd_numden")
+        return nd
+
+    def ccd_apply(self, shard, state, r, mode, nd, reg):
+        import ctypes
+
+        from . import _lib
+        from .optim import _stream
+        cp, _keep, ptrs = self._ccd_ptrs(state, r)
+        tmp = state["tmp"][mode]
+        _lib.check(_lib.load().cpfit_ccd_apply(
+            shard.device_pattern().handle, mode, ptrs, ctypes.c_void_p(cp[mode].data_ptr()),
+            ctypes.c_void_p(nd.data_ptr()), float(reg), ctypes.c_void_p(tmp.data_ptr()),
+            ctypes.c_void_p(state["resid"].data_ptr()), _stream()), "ccd_apply")
+        cp[mode].copy_(tmp)
+
+    def ccd_end(self, state, factors):
+        for n, c in enumerate(state["cols"]):
+            factors[n] = c.t().contiguous()
+
+    # -- SGD --
+    def sgd_grads(self, shard, factors, rate, rng, counter_offset):
+        from .optim import _sgd_grads_device
+        grads, _ = _sgd_grads_device(shard, factors, rate, rng, factors[0].dtype,
+                                     counter_offset=counter_offset)
+        return grads
+
+    def sgd_apply(self, factors, grads, step, shrink):
+        from .optim import _sgd_apply_device
+        _sgd_apply_device(factors, grads, step, shrink)
 
     def to_comm(self, x):
         return x.contiguous()
@@ -169,5 +305,6 @@ def als_strong_scaling_rows(blocks):
     return max(sizes) / max(1, sum(sizes)) * len(sizes)
 
 
-__all__ = ["row_partition", "nnz_partition", "shard_keys", "ShardedALS", "DeviceBackend",
+__all__ = ["row_partition", "nnz_partition", "shard_keys", "ShardedALS", "ShardedCCD",
+           "ShardedSGD", "DeviceBackend",
            "pad_rows", "als_strong_scaling_rows", "math"]

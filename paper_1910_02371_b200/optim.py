@@ -385,43 +385,58 @@ def ccd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
 # ---------------------------------------------------------------------------
 # stochastic gradient descent
 
-def _sgd_ls_device(t: SparseTensor, F, cfg: SolverConfig, rng: RngState):
-    """One SGD step on device factors F (list of CUDA tensors, replaced)."""
+def _sgd_grads_device(t: SparseTensor, F, rate: float, rng: RngState, dtype,
+                      counter_offset: int = 0):
+    """Sample (global Philox counter starts at counter_offset) and the per-mode
+    least-squares gradients MTTKRP(2(m - t)) on the device; returns
+    (grads, sample nnz)."""
     torch = _torch()
     from .sampling import sample_tensor
-    dtype = F[0].dtype
     code = _dtype_code(dtype)
     L = _lib.load()
-    shrink = 2.0 * cfg.step * cfg.reg * cfg.sample_rate
-    sampled = sample_tensor(t, cfg.sample_rate, rng, dtype)
+    sampled = sample_tensor(t, rate, rng, dtype, counter_offset=counter_offset)
     rank = F[0].shape[1]
     if sampled.nnz == 0:
-        grads = [torch.zeros_like(f) for f in F]
-    else:
-        phi1 = tttp_affine(sampled, F, 2.0, -2.0, dtype)  # 2(m - t), losses.py:46
-        pat = sampled.device_pattern()
-        grads = []
-        for mode in range(t.order):
-            g = torch.empty((t.shape[mode], rank), dtype=dtype, device=F[0].device)
-            _lib.check(L.cpfit_mttkrp(pat.handle, mode, code, rank,
-                                      ctypes.c_void_p(phi1.data_ptr()), 0, _ptrs(F),
-                                      ctypes.c_void_p(g.data_ptr()), _stream()), "mttkrp")
-            grads.append(g)
-    new = []
+        return [torch.zeros((t.shape[m], rank), dtype=dtype, device=F[0].device)
+                for m in range(t.order)], 0
+    phi1 = tttp_affine(sampled, F, 2.0, -2.0, dtype)  # 2(m - t), losses.py:46
+    pat = sampled.device_pattern()
+    grads = []
     for mode in range(t.order):
-        out = torch.empty_like(F[mode])
+        g = torch.empty((t.shape[mode], rank), dtype=dtype, device=F[0].device)
+        _lib.check(L.cpfit_mttkrp(pat.handle, mode, code, rank,
+                                  ctypes.c_void_p(phi1.data_ptr()), 0, _ptrs(F),
+                                  ctypes.c_void_p(g.data_ptr()), _stream()), "mttkrp")
+        grads.append(g)
+    return grads, sampled.nnz
+
+
+def _sgd_apply_device(F, grads, step: float, shrink: float, check: bool = True):
+    """F[n] <- (F[n] - step*grad_n) - shrink*F[n] for every mode at once."""
+    torch = _torch()
+    L = _lib.load()
+    new = []
+    for mode, f in enumerate(F):
+        out = torch.empty_like(f)
         bad = ctypes.c_int(0)
-        _lib.check(L.cpfit_sgd_update(code, F[mode].numel(), ctypes.c_void_p(F[mode].data_ptr()),
-                                      ctypes.c_void_p(grads[mode].data_ptr()), float(cfg.step),
+        _lib.check(L.cpfit_sgd_update(_dtype_code(f.dtype), f.numel(), ctypes.c_void_p(f.data_ptr()),
+                                      ctypes.c_void_p(grads[mode].data_ptr()), float(step),
                                       float(shrink), ctypes.c_void_p(out.data_ptr()),
                                       ctypes.byref(bad), _stream()), "sgd_update")
-        if bad.value and sampled.nnz:
+        if bad.value and check:
             raise NumericalError(f"sgd update diverged on mode {mode}; the learning rate is "
                                  "too high for this sample rate")
         new.append(out)
-    for mode in range(t.order):
+    for mode in range(len(F)):
         F[mode] = new[mode]
-    return sampled.nnz
+
+
+def _sgd_ls_device(t: SparseTensor, F, cfg: SolverConfig, rng: RngState):
+    """One SGD step on device factors F (list of CUDA tensors, replaced)."""
+    shrink = 2.0 * cfg.step * cfg.reg * cfg.sample_rate
+    grads, n = _sgd_grads_device(t, F, cfg.sample_rate, rng, F[0].dtype)
+    _sgd_apply_device(F, grads, cfg.step, shrink, check=n > 0)
+    return n
 
 
 def sgd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,

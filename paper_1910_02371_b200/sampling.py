@@ -51,14 +51,17 @@ def gather_values(values, parent):
     return out
 
 
-def sample_tensor(t: SparseTensor, rate: float, rng, dtype=None) -> SparseTensor:
+def sample_tensor(t: SparseTensor, rate: float, rng, dtype=None,
+                  counter_offset: int = 0) -> SparseTensor:
+    """Bernoulli sample of t's entries; entry e uses Philox draw
+    counter_offset + e (a nonzero shard passes its first global index)."""
     if not 0.0 < rate <= 1.0:
         raise ValueError(f"sample rate must be in (0, 1], got {rate}")
     import torch
     dtype = dtype or torch.float64
     if t.nnz == 0:
         return SparseTensor(t.shape, np.empty(0, np.uint64), np.empty(0), validate=False)
-    pat, parent = sample_pattern(t, rate, rng)
+    pat, parent = sample_pattern(t, rate, rng, counter_offset)
     vals = gather_values(t.device_values(dtype), parent)
     shared = _Shared(pattern=pat, task_size=t._shared.task_size, parent=parent)
     host_parent = {}

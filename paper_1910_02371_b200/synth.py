@@ -177,11 +177,13 @@ def cfg3_device(seed: int = CFG3_SEED, nnz: int = 100_480_507,
 
 
 def cfg5_device(seed: int = CFG5_SEED, nnz: int = 1_000_000_000,
-                shape=(100_000, 100_000, 100_000, 1_000), rank: int = 64, device="cuda"):
+                shape=(100_000, 100_000, 100_000, 1_000), rank: int = 64, device="cuda",
+                with_keys: bool = False):
     """BASELINE cfg 5 synthesised on the GPU: order 4, nnz distinct uniform
     keys, values = rank-8 CP model (truth factors N(0, 1/8), evaluated with
     the library's own TTTP kernel) + N(0, 0.1) noise, fp32; R=64 factors
-    N(0, 1/R).  Returns (shape, sorted int64 keys, f32 values, f32 factors)."""
+    N(0, 1/R).  Returns (shape, tensor, f32 values, f32 factors) and, with
+    ``with_keys``, the sorted int64 device keys as a fifth item."""
     import torch
     shape = tuple(int(d) for d in shape)
     space = 1
@@ -206,4 +208,6 @@ def cfg5_device(seed: int = CFG5_SEED, nnz: int = 1_000_000_000,
     from .losses import tttp_affine
     t = SparseTensor.from_device(shape, keys, noise)
     values = tttp_affine(t, truth, 1.0, 1.0, torch.float32)  # model + noise
+    if with_keys:
+        return shape, t, values, factors, keys
     return shape, t, values, factors

@@ -3,7 +3,9 @@ paper_1910_02371_b200.dist, with the CPU oracle as the row-local compute:
 the row-sharded ALS sweep with an all-gather of factor rows must reproduce
 the single-process sweep bit for bit; the nonzero-sharded SGD sample must be
 the single-process sample bit for bit and the all-reduced gradients must
-match within 1e-12."""
+match within 1e-12; the nonzero-sharded CCD++ sweep and SGD steps must match
+the single-process sweeps within 1e-10 / 1e-12 (the all-reduce reassociates
+the per-row sums) with the replicas bit-identical."""
 
 import os
 import socket
@@ -43,6 +45,55 @@ class OracleBackend:
 
     def cat(self, parts):
         return torch.cat(parts, 0)
+
+    # nonzero shards (ShardedCCD / ShardedSGD)
+    def make_nnz_shard(self, shape, keys, values):
+        return self.make_shard(shape, keys, values)
+
+    def ccd_begin(self, shard, factors):
+        model = O.tttp(shard.with_values(np.ones(shard.nnz)), factors)
+        return {"cols": [np.ascontiguousarray(f.T) for f in factors],
+                "resid": shard.values - model, "coords": shard.coords()}
+
+    def ccd_numden(self, shard, st, r, mode):
+        c = st["coords"]
+        part = np.ones(shard.nnz)
+        for q in range(shard.order):
+            if q != mode:
+                part = part * st["cols"][q][r][c[q]]
+        rho = st["resid"] + part * st["cols"][mode][r][c[mode]]
+        st["part"], st["rho"] = part, rho
+        d = shard.shape[mode]
+        return torch.from_numpy(np.concatenate([
+            np.bincount(c[mode], weights=rho * part, minlength=d),
+            np.bincount(c[mode], weights=part * part, minlength=d)]))
+
+    def ccd_apply(self, shard, st, r, mode, nd, reg):
+        d = shard.shape[mode]
+        nd = nd.numpy()
+        old = st["cols"][mode][r]
+        dr = nd[d:] + reg
+        new = np.where(dr > 0.0, nd[:d] / np.where(dr > 0.0, dr, 1.0), old)
+        st["resid"] = st["rho"] - st["part"] * new[st["coords"][mode]]
+        st["cols"][mode][r] = new
+
+    def ccd_end(self, st, factors):
+        for n, c in enumerate(st["cols"]):
+            factors[n] = np.ascontiguousarray(c.T)
+
+    def sgd_grads(self, shard, factors, rate, rng, counter_offset):
+        seed, path = rng
+        kept = np.flatnonzero(O.uniform(seed, path, shard.nnz, start=counter_offset) < rate)
+        s = O.OTensor(shard.shape, shard.keys[kept], shard.values[kept])
+        if s.nnz == 0:
+            return [torch.zeros(f.shape, dtype=torch.float64) for f in factors]
+        model = O.tttp(s.with_values(np.ones(s.nnz)), factors)
+        phi1 = s.with_values(2.0 * (model - s.values))
+        return [torch.from_numpy(O.mttkrp(phi1, factors, m)) for m in range(s.order)]
+
+    def sgd_apply(self, factors, grads, step, shrink):
+        for m in range(len(factors)):
+            factors[m] = (factors[m] - step * grads[m].numpy()) - shrink * factors[m]
 
 
 def _instance(nnz=20_000):
@@ -97,6 +148,17 @@ def _worker(rank, world, port, outdir):
             dist.all_reduce(tg)
             summed.append(tg.numpy())
         np.savez(os.path.join(outdir, f"sgd{rank}.npz"), kept=kept_local, *summed)
+        # CCD++: nonzero shards, all-reduced (num, den) per (r, mode)
+        ccd = D.ShardedCCD(keys, values, shape, 1e-5, OracleBackend())
+        fs = [f.copy() for f in factors]
+        ccd.sweep(fs)
+        np.savez(os.path.join(outdir, f"ccd{rank}.npz"), *fs)
+        # SGD steps through ShardedSGD
+        sgd = D.ShardedSGD(keys, values, shape, OracleBackend())
+        fs = [f.copy() for f in factors]
+        for it in range(2):
+            sgd.step(fs, 0.3, 1e-3, 1e-4, (7, (1, it)))
+        np.savez(os.path.join(outdir, f"sgdsteps{rank}.npz"), *fs)
     finally:
         dist.destroy_process_group()
 
@@ -158,3 +220,30 @@ def test_sharded_sgd_sample_and_gradients(dist_run):
         got = z0[f"arr_{m}"]
         assert np.array_equal(got, z1[f"arr_{m}"])
         assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_sharded_ccd_matches_single_process(dist_run):
+    shape, keys, values, factors = _instance()
+    ot = O.OTensor(shape, keys, values)
+    fs = [f.copy() for f in factors]
+    O.ccd_sweep(ot, fs, 1e-5)
+    z0 = np.load(os.path.join(dist_run, "ccd0.npz"))
+    z1 = np.load(os.path.join(dist_run, "ccd1.npz"))
+    for n in range(3):
+        got = z0[f"arr_{n}"]
+        assert np.array_equal(got, z1[f"arr_{n}"])  # replicas agree bit for bit
+        assert np.linalg.norm(got - fs[n]) <= 1e-10 * np.linalg.norm(fs[n]), n
+
+
+def test_sharded_sgd_steps_match_single_process(dist_run):
+    shape, keys, values, factors = _instance()
+    ot = O.OTensor(shape, keys, values)
+    fs = [f.copy() for f in factors]
+    for it in range(2):
+        O.sgd_sweep(ot, fs, 1e-4, 1e-3, 0.3, 7, (1, it))
+    z0 = np.load(os.path.join(dist_run, "sgdsteps0.npz"))
+    z1 = np.load(os.path.join(dist_run, "sgdsteps1.npz"))
+    for n in range(3):
+        got = z0[f"arr_{n}"]
+        assert np.array_equal(got, z1[f"arr_{n}"])
+        assert np.linalg.norm(got - fs[n]) <= 1e-12 * np.linalg.norm(fs[n]), n
