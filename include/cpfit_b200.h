@@ -147,6 +147,16 @@ int cpfit_als_update(cpfit_pattern *p, int mode, int dtype, int rank,
                      void *gram_out, void *rhs_out, int64_t *bad_row,
                      void *stream);
 
+/* TTTP whose result is also delivered to HOST memory (the reference's
+ * numpy-returning tttp, kernels.py:105-149): the nonzeros are processed in
+ * chunks (chunk <= 0: nnz/8, at most 16 chunks) and each chunk is copied
+ * into host_out (pinned memory for an asynchronous DMA) while the next one
+ * computes.  dev_out receives the device copy.  Asynchronous on `stream`:
+ * host_out is complete once `stream` is synchronised. */
+int cpfit_tttp_host(cpfit_pattern *p, int dtype, int rank, const void *vals,
+                    const void *const *factors, void *dev_out, void *host_out,
+                    int64_t chunk, void *stream);
+
 /* TTTP with an affine epilogue: out[e] = alpha * m_e + beta * vals[e], with
  * m_e = sum_r prod_n factors[n][i_n(e), r].  alpha = 2, beta = -2 gives the
  * least-squares derivative tensor 2(m - t) (losses.py:41-48, model via
@@ -180,6 +190,11 @@ int cpfit_gather_values(int dtype, int64_t n, const int32_t *idx,
  * Serves objective / rmse (losses.py:126-150, optim.py:642-652). */
 int cpfit_reduce(int op, int dtype, int64_t n, const void *x, const void *y,
                  double *result, void *stream);
+
+/* Device-side factor validation (validation.py:47-59): *flag (a DEVICE int,
+ * zeroed by the caller) is OR-ed with 1 if any of the n elements is NaN or
+ * infinite.  Asynchronous: read the flag after synchronising the stream. */
+int cpfit_check_finite(int dtype, int64_t n, const void *x, int *flag, void *stream);
 
 /* SGD step out = (a - step*grad) - shrink*a in numpy's evaluation order
  * (optim.py:313-330); *nonfinite = 1 if any result is not finite. */

@@ -36,7 +36,8 @@ SYMBOLS = (
     "cpfit_tttp_axpby", "cpfit_sample", "cpfit_pattern_parent_index", "cpfit_gather_values",
     "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_update", "cpfit_probe_gather",
     "cpfit_solve_rows", "cpfit_dense_reduce", "cpfit_khatri_rao", "cpfit_als_update",
-    "cpfit_ccd_numden", "cpfit_ccd_apply",
+    "cpfit_ccd_numden", "cpfit_ccd_apply", "cpfit_check_finite",
+    "cpfit_tttp_host",
 )
 
 _vp = ctypes.c_void_p
@@ -91,6 +92,8 @@ def load(path: str | None = None):
         "cpfit_sgd_update": [_int, _i64, _vp, _vp, ctypes.c_double, ctypes.c_double, _vp,
                              ctypes.POINTER(_int), _vp],
         "cpfit_ccd_update": [_vp, _int, _PP, _vp, _vp, _vp, ctypes.c_double, _vp],
+        "cpfit_tttp_host": [_vp, _int, _int, _vp, _PP, _vp, _vp, _i64, _vp],
+        "cpfit_check_finite": [_int, _i64, _vp, _vp, _vp],
         "cpfit_ccd_numden": [_vp, _int, _PP, _vp, _vp, _vp, _vp],
         "cpfit_ccd_apply": [_vp, _int, _PP, _vp, _vp, ctypes.c_double, _vp, _vp, _vp],
         "cpfit_probe_gather": [_vp, _int, _int, _PP, _i64, _vp, _i64, _vp],

@@ -231,6 +231,19 @@ __global__ void sgd_update_kernel(int64_t n, const T *__restrict__ a, const T *_
   if (bad && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+// Factor validation on the device (validation.py:47-59 "contains non-finite
+// entries"): *flag |= 1 if any element is NaN/Inf.  The caller reads the flag
+// after its own result synchronisation, so the check costs no extra host pass.
+template <typename T>
+__global__ void check_finite_kernel(int64_t n, const T *__restrict__ x, int *flag) {
+  int bad = 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[k]);
+  bad = __syncthreads_or(bad);
+  if (bad && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 }  // namespace cpfit
 
 using namespace cpfit;
@@ -330,6 +343,19 @@ int cpfit_reduce(int op, int dtype, int64_t n, const void *x, const void *y, dou
     return run_reduce<float>(op, n, (const float *)x, (const float *)y, result, s);
   set_error("unknown dtype %d", dtype);
   return CPFIT_EINVAL;
+}
+
+int cpfit_check_finite(int dtype, int64_t n, const void *x, int *flag, void *stream) {
+  if (n <= 0) return CPFIT_OK;
+  if (!x || !flag) { set_error("null argument"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64)
+    check_finite_kernel<double><<<grid_for(n, 256, 2), 256, 0, s>>>(n, (const double *)x, flag);
+  else if (dtype == CPFIT_F32)
+    check_finite_kernel<float><<<grid_for(n, 256, 2), 256, 0, s>>>(n, (const float *)x, flag);
+  else { set_error("unknown dtype %d", dtype); return CPFIT_EINVAL; }
+  CPFIT_LAUNCH_CHECK("check_finite");
+  return CPFIT_OK;
 }
 
 int cpfit_sgd_update(int dtype, int64_t n, const void *a, const void *grad, double step,

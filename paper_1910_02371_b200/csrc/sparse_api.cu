@@ -14,20 +14,21 @@ extern template int dispatch_mttkrp<float>(const MttkrpParams<float> &, int, cud
 template <typename T>
 static int run_tttp(cpfit_pattern *pt, int rank, const void *vals, const void *const *factors,
                     void *out, cudaStream_t s, int epi = 0, double alpha = 0.0,
-                    double beta = 0.0) {
+                    double beta = 0.0, int64_t begin = 0, int64_t end = -1) {
+  if (end < 0) end = pt->nnz;
   TttpParams<T> p{};
   p.epi = epi;
   p.alpha = (T)alpha;
   p.beta = (T)beta;
   p.rank = rank;
-  p.nnz = pt->nnz;
-  p.vals = (const T *)vals;
-  p.out = (T *)out;
+  p.nnz = end - begin;
+  p.vals = (const T *)vals + begin;
+  p.out = (T *)out + begin;
   int np = 0;
   const void *ptrs[CPFIT_MAXN];
   for (int n = 0; n < pt->order; ++n) {
     if (!factors[n]) continue;
-    p.idx[np] = pt->coords[n];
+    p.idx[np] = pt->coords[n] + begin;
     p.fac[np] = (const T *)factors[n];
     ptrs[np] = factors[n];
     ++np;
@@ -37,8 +38,45 @@ static int run_tttp(cpfit_pattern *pt, int rank, const void *vals, const void *c
     return CPFIT_EINVAL;
   }
   p.np = np;
-  if (pt->nnz == 0) return CPFIT_OK;
+  if (p.nnz <= 0) return CPFIT_OK;
   return dispatch_tttp<T>(p, pick_vec<T>(rank, ptrs, np), s);
+}
+
+// Chunked TTTP whose chunks are copied to host memory while later chunks
+// compute: chunk c's copy (on a library-owned copy stream) waits on an event
+// recorded after chunk c's kernel, and `s` finally waits on the copy stream,
+// so synchronising `s` covers results on both sides.
+template <typename T>
+static int run_tttp_host(cpfit_pattern *pt, int rank, const void *vals,
+                         const void *const *factors, void *dev_out, void *host_out,
+                         int64_t chunk, cudaStream_t s) {
+  static cudaStream_t copy_stream[64] = {};
+  static cudaEvent_t evs[64][17] = {};
+  int dev = 0;
+  CPFIT_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) { set_error("device index %d unsupported", dev); return CPFIT_EINVAL; }
+  if (!copy_stream[dev]) {
+    CPFIT_CUDA(cudaStreamCreateWithFlags(&copy_stream[dev], cudaStreamNonBlocking));
+    for (int k = 0; k < 17; ++k)
+      CPFIT_CUDA(cudaEventCreateWithFlags(&evs[dev][k], cudaEventDisableTiming));
+  }
+  const int64_t nnz = pt->nnz;
+  if (chunk <= 0) chunk = (nnz + 7) / 8;
+  if ((nnz + chunk - 1) / chunk > 16) chunk = (nnz + 15) / 16;
+  chunk = (chunk + 31) & ~int64_t(31);
+  cudaStream_t cs = copy_stream[dev];
+  int k = 0;
+  for (int64_t b = 0; b < nnz; b += chunk, ++k) {
+    const int64_t e = b + chunk < nnz ? b + chunk : nnz;
+    CPFIT_TRY(run_tttp<T>(pt, rank, vals, factors, dev_out, s, 0, 0.0, 0.0, b, e));
+    CPFIT_CUDA(cudaEventRecord(evs[dev][k], s));
+    CPFIT_CUDA(cudaStreamWaitEvent(cs, evs[dev][k], 0));
+    CPFIT_CUDA(cudaMemcpyAsync((T *)host_out + b, (const T *)dev_out + b, (e - b) * sizeof(T),
+                               cudaMemcpyDeviceToHost, cs));
+  }
+  CPFIT_CUDA(cudaEventRecord(evs[dev][16], cs));
+  CPFIT_CUDA(cudaStreamWaitEvent(s, evs[dev][16], 0));
+  return CPFIT_OK;
 }
 
 template <typename T>
@@ -102,6 +140,21 @@ int cpfit_tttp(cpfit_pattern *p, int dtype, int rank, const void *vals,
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == CPFIT_F64) return run_tttp<double>(p, rank, vals, factors, out, s);
   if (dtype == CPFIT_F32) return run_tttp<float>(p, rank, vals, factors, out, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+int cpfit_tttp_host(cpfit_pattern *p, int dtype, int rank, const void *vals,
+                    const void *const *factors, void *dev_out, void *host_out, int64_t chunk,
+                    void *stream) {
+  if (!p) { set_error("null pattern"); return CPFIT_EINVAL; }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  if (p->nnz > 0 && (!dev_out || !host_out)) { set_error("null output"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64)
+    return run_tttp_host<double>(p, rank, vals, factors, dev_out, host_out, chunk, s);
+  if (dtype == CPFIT_F32)
+    return run_tttp_host<float>(p, rank, vals, factors, dev_out, host_out, chunk, s);
   set_error("unknown dtype %d", dtype);
   return CPFIT_EINVAL;
 }

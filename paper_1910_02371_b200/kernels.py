@@ -56,7 +56,55 @@ def _to_device(a, dtype):
         return None
     if _is_torch(a):
         return a.to(device=cuda_device(), dtype=dtype).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(a)).to(cuda_device()).to(dtype)
+    # non_blocking: pinned sources copy asynchronously; pageable ones are
+    # staged by the driver before the call returns (safe to reuse either way)
+    return torch.from_numpy(np.ascontiguousarray(a)).to(cuda_device(), non_blocking=True) \
+        .to(dtype)
+
+
+def _checked_factor_list(factors, dims, **kw):
+    """check_factor_list with the non-finite scan deferred to the device.
+    On a host-side (shape / rank) error the full host validation re-runs so
+    the first error raised is the reference's (validation.py:62-95 order)."""
+    try:
+        return check_factor_list(factors, dims, finite=False, **kw)
+    except ValueError:
+        check_factor_list(factors, dims, finite=True, **kw)
+        raise
+
+
+class _FiniteCheck:
+    """Deferred 'contains non-finite entries' check (validation.py:57-58):
+    one cpfit_check_finite launch per uploaded operand into a device flag
+    array; ``raise_if_bad`` reads the flags after the call's own result
+    synchronisation and raises the reference's ValueError for the first bad
+    operand (the computed result is discarded)."""
+
+    def __init__(self, named):
+        torch = _torch()
+        self.named = [(n, d) for n, d in named if d is not None and d.numel()]
+        self.flags = None
+        if not self.named:
+            return
+        self.flags = torch.zeros(len(self.named), dtype=torch.int32, device=cuda_device())
+        L = _lib.load()
+        base = self.flags.data_ptr()
+        for k, (_, d) in enumerate(self.named):
+            _lib.check(L.cpfit_check_finite(_dtype_code(d.dtype), d.numel(), _vp(d),
+                                            ctypes.c_void_p(base + 4 * k), _stream()),
+                       "check_finite")
+
+    def raise_if_bad(self):
+        if self.flags is None:
+            return
+        bad = to_host(self.flags)
+        for k, (name, _) in enumerate(self.named):
+            if bad[k]:
+                raise ValueError(f"{name} contains non-finite entries")
+
+
+def _named(factors, dev):
+    return [(f"factor[{n}]", d) for n, d in enumerate(dev) if factors[n] is not None]
 
 
 def _ptrs(tensors):
@@ -80,11 +128,12 @@ def mttkrp(t: SparseTensor, factors, mode: int, threads: int = 1):
     other modes of factor[i_n, r]; rows with no entries are exactly zero.
     """
     mode = check_mode(mode, t.order)
-    factors, rank = check_factor_list(factors, t.shape, skip_mode=mode)
+    factors, rank = _checked_factor_list(factors, t.shape, skip_mode=mode)
     dtype = _compute_dtype(factors)
     on_device = _device_mode(factors)
     torch = _torch()
     dev = [_to_device(f, dtype) for f in factors]
+    fin = _FiniteCheck(_named(factors, dev))
     out = torch.empty((t.shape[mode], rank), dtype=dtype, device=cuda_device())
     if t.nnz == 0:
         out.zero_()
@@ -93,7 +142,9 @@ def mttkrp(t: SparseTensor, factors, mode: int, threads: int = 1):
         _lib.check(_lib.load().cpfit_mttkrp(
             t.device_pattern().handle, mode, _dtype_code(dtype), rank, _vp(vals), 1,
             _ptrs(dev), _vp(out), _stream()), "mttkrp")
-    return out if on_device else to_host(out)
+    res = out if on_device else to_host(out)
+    fin.raise_if_bad()
+    return res
 
 
 def _tttp_slices(rank: int, h_slices, nnz: int, budget_bytes: int):
@@ -115,19 +166,34 @@ def tttp(t: SparseTensor, factors, h_slices: int | None = None,
     factors[n][coords[n][e], r]; None slots are skipped.  One fused pass:
     ``h_slices`` is validated but no nnz x R intermediate ever exists.
     """
-    factors, rank = check_factor_list(factors, t.shape, allow_missing=True)
+    factors, rank = _checked_factor_list(factors, t.shape, allow_missing=True)
     if t.nnz == 0:
+        check_factor_list(factors, t.shape, allow_missing=True)  # host finiteness scan
         return t
     _tttp_slices(rank, h_slices, t.nnz, budget_bytes)
     dtype = _compute_dtype(factors)
+    on_device = _device_mode(factors)
     torch = _torch()
     dev = [_to_device(f, dtype) for f in factors]
+    fin = _FiniteCheck(_named(factors, dev))
     vals = t.device_values(dtype)
     out = torch.empty(t.nnz, dtype=dtype, device=cuda_device())
-    _lib.check(_lib.load().cpfit_tttp(
-        t.device_pattern().handle, _dtype_code(dtype), rank, _vp(vals), _ptrs(dev),
-        _vp(out), _stream()), "tttp")
-    return t.with_values(out)
+    res = t.with_values(out)
+    if on_device:
+        _lib.check(_lib.load().cpfit_tttp(
+            t.device_pattern().handle, _dtype_code(dtype), rank, _vp(vals), _ptrs(dev),
+            _vp(out), _stream()), "tttp")
+    else:
+        # numpy operands: the reference returns host values -- chunked kernel
+        # with the device->host DMA of each chunk overlapping the next chunk
+        host = torch.empty(t.nnz, dtype=dtype, pin_memory=True)
+        _lib.check(_lib.load().cpfit_tttp_host(
+            t.device_pattern().handle, _dtype_code(dtype), rank, _vp(vals), _ptrs(dev),
+            _vp(out), _vp(host), 0, _stream()), "tttp_host")
+        torch.cuda.current_stream().synchronize()
+        res._values = host.numpy()
+    fin.raise_if_bad()
+    return res
 
 
 def sddmm(s: SparseTensor, u, v, threads: int = 1) -> SparseTensor:

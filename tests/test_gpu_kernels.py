@@ -345,3 +345,29 @@ def test_fused_als_update_vs_oracle(rank):
             # run-to-run bitwise
             x2 = _als_mode_device(t, F, mode, 1e-3)
             assert torch.equal(x, x2)
+
+
+def test_nonfinite_factors_raise_like_reference():
+    """validation.py:57-58: 'factor[n] contains non-finite entries' -- checked
+    on the device after upload (cpfit_check_finite), same first error as the
+    reference's host-order validation."""
+    torch = _torch()
+    t = cp.build_tensor([((0, 0, 0), 1.0), ((1, 1, 1), 2.0)], (2, 2, 2))
+    good = np.ones((2, 3))
+    bad = good.copy()
+    bad[1, 2] = np.nan
+    with pytest.raises(ValueError, match=r"factor\[1\] contains non-finite"):
+        cp.mttkrp(t, [None, bad, good], 0)
+    inf = good.copy()
+    inf[0, 0] = np.inf
+    with pytest.raises(ValueError, match=r"factor\[2\] contains non-finite"):
+        cp.tttp(t, [good, good, inf])
+    with pytest.raises(ValueError, match=r"factor\[1\] contains non-finite"):
+        cp.mttkrp(t, [None, torch.from_numpy(bad).cuda(), torch.from_numpy(good).cuda()], 0)
+    # first error in the reference's order: factor[0] non-finite before factor[2]'s shape
+    with pytest.raises(ValueError, match=r"factor\[0\] contains non-finite"):
+        cp.tttp(t, [bad, good, np.ones((3, 3))])
+    with pytest.raises(ValueError, match=r"factor\[2\] has 3 rows"):
+        cp.tttp(t, [good, good, np.ones((3, 3))])
+    # valid calls still work after a rejected one
+    assert cp.tttp(t, [good, good, good]).values.tolist() == [3.0, 6.0]
