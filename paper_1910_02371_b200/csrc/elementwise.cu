@@ -30,14 +30,19 @@ __device__ __forceinline__ void philox4x64_10(uint64_t c0, uint64_t key0, uint64
 }
 
 constexpr int SMP_THREADS = 256;
-constexpr int SMP_BLOCKS_PER_THREAD = 4;  // Philox blocks (4 draws each) per thread
-constexpr int64_t SMP_TILE = (int64_t)SMP_THREADS * SMP_BLOCKS_PER_THREAD * 4;
+constexpr int SMP_BLOCKS_PER_THREAD = 8;  // Philox blocks (4 draws each) per thread: 32 bits
+
+// u = (w >> 11) * 2^-53 < rate  <=>  (w >> 11) < ceil(rate * 2^53): scaling by a
+// power of two is exact, so the integer test decides exactly like numpy's
+// double comparison.
+__host__ __device__ inline uint64_t sample_threshold(double rate) {
+  return (uint64_t)ceil(rate * 9007199254740992.0);
+}
 
 // keep-bits of the draws of local entries [4*b - phase, ...): one Philox call
-// serves 4 consecutive global entries.  Returns the number kept by this
-// thread and the bit mask (bit j*4+w = local entry of block j, word w).
+// serves 4 consecutive global entries.  Bit j*4+w = word w of block j.
 __device__ __forceinline__ uint32_t sample_bits(int64_t tile, int64_t n, int64_t off,
-                                                uint64_t key0, uint64_t key1, double rate,
+                                                uint64_t key0, uint64_t key1, uint64_t thr,
                                                 int64_t *first_local) {
   // global philox blocks covering local [0, n): g = off .. off + n - 1
   const int64_t gb0 = off >> 2;  // first global block
@@ -54,20 +59,22 @@ __device__ __forceinline__ uint32_t sample_bits(int64_t tile, int64_t n, int64_t
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t l = lb + q;
-      const double u = (double)(w[q] >> 11) * (1.0 / 9007199254740992.0);
-      if (l >= 0 && l < n && u < rate) bits |= 1u << (j * 4 + q);
+      if (l >= 0 && l < n && (w[q] >> 11) < thr) bits |= 1u << (j * 4 + q);
     }
   }
   return bits;
 }
 
+// Pass 1 (the only Philox pass): keep-masks, one 32-bit word per thread and
+// tile, plus per-tile survivor counts.
 __global__ void __launch_bounds__(SMP_THREADS)
-sample_count_kernel(int64_t n, int64_t off, uint64_t key0, uint64_t key1, double rate,
-                    int64_t ntiles, int64_t *tile_counts) {
+sample_count_kernel(int64_t n, int64_t off, uint64_t key0, uint64_t key1, uint64_t thr,
+                    int64_t ntiles, int64_t *tile_counts, uint32_t *__restrict__ masks) {
   __shared__ int warp_tot[SMP_THREADS / 32];
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     int64_t fl;
-    const uint32_t bits = sample_bits(tile, n, off, key0, key1, rate, &fl);
+    const uint32_t bits = sample_bits(tile, n, off, key0, key1, thr, &fl);
+    masks[tile * SMP_THREADS + threadIdx.x] = bits;
     int c = __popc(bits);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -82,15 +89,18 @@ sample_count_kernel(int64_t n, int64_t off, uint64_t key0, uint64_t key1, double
   }
 }
 
+// Pass 2: compaction driven by the stored masks (no Philox recomputation).
 __global__ void __launch_bounds__(SMP_THREADS)
-sample_select_kernel(int64_t n, int64_t off, uint64_t key0, uint64_t key1, double rate,
-                     int64_t ntiles, const int64_t *__restrict__ tile_offsets,
-                     int32_t *__restrict__ kept) {
+sample_select_kernel(int64_t n, int64_t off, int64_t ntiles,
+                     const int64_t *__restrict__ tile_offsets,
+                     const uint32_t *__restrict__ masks, int32_t *__restrict__ kept) {
   __shared__ int warp_pre[SMP_THREADS / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    int64_t fl;
-    uint32_t bits = sample_bits(tile, n, off, key0, key1, rate, &fl);
+    const int64_t b = (off >> 2) + tile * (SMP_THREADS * SMP_BLOCKS_PER_THREAD) +
+                      (int64_t)threadIdx.x * SMP_BLOCKS_PER_THREAD;
+    const int64_t fl = b * 4 - off;
+    uint32_t bits = masks[tile * SMP_THREADS + threadIdx.x];
     const int c = __popc(bits);
     int incl = c;
 #pragma unroll
@@ -266,22 +276,25 @@ int cpfit_sample(cpfit_pattern *src, uint64_t key0, uint64_t key1, int64_t count
   const int64_t per_tile = (int64_t)SMP_THREADS * SMP_BLOCKS_PER_THREAD;
   const int64_t ntiles = (nblk + per_tile - 1) / per_tile;
   Scratch<int64_t> counts(s), offs(s);
+  Scratch<uint32_t> masks(s);
   int64_t total = 0;
   int32_t *kept = nullptr;
   if (ntiles > 0) {
     CPFIT_TRY(counts.alloc(ntiles));
     CPFIT_TRY(offs.alloc(ntiles + 1));
+    CPFIT_TRY(masks.alloc((size_t)ntiles * SMP_THREADS));
     unsigned grid = (unsigned)(ntiles < (int64_t)num_sms() * 16 ? ntiles : num_sms() * 16);
-    sample_count_kernel<<<grid, SMP_THREADS, 0, s>>>(n, counter_offset, key0, key1, rate,
-                                                    ntiles, counts.ptr);
+    sample_count_kernel<<<grid, SMP_THREADS, 0, s>>>(n, counter_offset, key0, key1,
+                                                    sample_threshold(rate), ntiles, counts.ptr,
+                                                    masks.ptr);
     CPFIT_LAUNCH_CHECK("sample_count");
     CPFIT_TRY(exclusive_scan<int64_t>(counts.ptr, offs.ptr, ntiles, s));
     CPFIT_CUDA(cudaMemcpyAsync(&total, offs.ptr + ntiles, sizeof(int64_t),
                                cudaMemcpyDeviceToHost, s));
     CPFIT_CUDA(cudaStreamSynchronize(s));
     CPFIT_TRY(dalloc(&kept, total > 0 ? total : 1, s));
-    sample_select_kernel<<<grid, SMP_THREADS, 0, s>>>(n, counter_offset, key0, key1, rate,
-                                                     ntiles, offs.ptr, kept);
+    sample_select_kernel<<<grid, SMP_THREADS, 0, s>>>(n, counter_offset, ntiles, offs.ptr,
+                                                     masks.ptr, kept);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { dfree(kept, s); return cuda_status(e, "sample_select"); }
   } else {
