@@ -166,6 +166,20 @@ int cpfit_tttp_axpby(cpfit_pattern *p, int dtype, int rank, const void *vals,
                      const void *const *factors, double alpha, double beta,
                      void *out, void *stream);
 
+/* ---- second-order step (optim.py:348-598, gn_step / hessian_matvec) ---- */
+
+/* out[e] = w[e] * sum_d sum_r x_d[i_d(e), r] * prod_{p != d} factors[p][i_p(e), r]:
+ * the sum over d of the TTTPs with slot d substituted by its update block
+ * (hessian_matvec's z, optim.py:372-376), one gather of the 2N rows per
+ * entry.  w nullable (unit weights); every factor and block is required. */
+int cpfit_tttp_subst(cpfit_pattern *p, int dtype, int rank, const void *w,
+                     const void *const *factors, const void *const *xblocks,
+                     void *out, void *stream);
+
+/* out[k] = a * x[k] + b * y[k] (PCG vector updates, optim.py:513-531). */
+int cpfit_axpby(int dtype, int64_t n, double a, const void *x, double b,
+                const void *y, void *out, void *stream);
+
 /* ---- sampling (SparseTensor.sample, core.py:173-183) ------------------ */
 
 /* Keep entry e iff u_e < rate where u_e is draw (counter_offset + e) of

@@ -371,3 +371,135 @@ def objective_ls(t: OTensor, factors, reg: float) -> float:
     if reg:
         total += reg * sum(float(np.sum(f * f)) for f in factors)
     return total
+
+
+# ---------------------------------------------------------------------------
+# second-order step (optim.py:334-598), restated on the oracle kernels.
+# Losses are given as (dphi, d2phi) callables of (t, m) (losses.py:41-104).
+
+def loss_derivs(ident: str):
+    """losses.py:41-79: least squares and Poisson log link (m clamped at 50)."""
+    if ident == "ls":
+        return (lambda tv, m: 2.0 * (m - tv),
+                lambda tv, m: np.full_like(np.asarray(m, dtype=np.float64), 2.0))
+    if ident == "poisson":
+        def ex(m):
+            return np.exp(np.minimum(np.asarray(m, dtype=np.float64), 50.0))
+        return (lambda tv, m: ex(m) - tv, lambda tv, m: ex(m))
+    raise OracleError("loss", ident)
+
+
+def gradient_blocks(t: OTensor, factors, ident: str, reg: float):
+    """optim.py:336-345."""
+    dphi, _ = loss_derivs(ident)
+    model = tttp(t.with_values(np.ones(t.nnz)), factors)
+    phi1 = t.with_values(dphi(t.values, model))
+    return [mttkrp(phi1, factors, d) + 2.0 * reg * factors[d] for d in range(t.order)]
+
+
+def hessian_matvec(phi1: OTensor, phi2: OTensor, factors, x_blocks, variant: str,
+                   reg: float):
+    """optim.py:348-384 (composed form: N substituted TTTPs, one MTTKRP per mode,
+    Newton cross terms as MTTKRPs of phi1 with one substituted slot)."""
+    n = len(factors)
+    z = np.zeros(phi2.nnz)
+    for p in range(n):
+        sub = list(factors)
+        sub[p] = x_blocks[p]
+        z += tttp(phi2, sub)
+    zt = phi2.with_values(z)
+    y = [mttkrp(zt, factors, d) + 2.0 * reg * x_blocks[d] for d in range(n)]
+    if variant == "newton":
+        for d in range(n):
+            for p in range(n):
+                if p != d:
+                    sub = list(factors)
+                    sub[p] = x_blocks[p]
+                    y[d] += mttkrp(phi1, sub, d)
+    return y
+
+
+def _bdot(a, b) -> float:
+    return float(sum(np.sum(x * y) for x, y in zip(a, b)))
+
+
+def pcg(matvec, precond, rhs, rel_tol: float, max_iters: int):
+    """optim.py:492-531."""
+    x = [np.zeros_like(b) for b in rhs]
+    r = [b.copy() for b in rhs]
+    b_norm = math.sqrt(_bdot(rhs, rhs))
+    if b_norm == 0.0:
+        return x, 0
+    z = precond(r)
+    p = [zi.copy() for zi in z]
+    rz = _bdot(r, z)
+    for it in range(1, max_iters + 1):
+        ap = matvec(p)
+        p_ap = _bdot(p, ap)
+        if not math.isfinite(p_ap):
+            raise OracleError("cg_curvature")
+        if p_ap <= 0.0:
+            return x, it - 1
+        alpha = rz / p_ap
+        for d in range(len(x)):
+            x[d] += alpha * p[d]
+            r[d] -= alpha * ap[d]
+        res = math.sqrt(_bdot(r, r))
+        if res / b_norm < rel_tol:
+            return x, it
+        z = precond(r)
+        rz_new = _bdot(r, z)
+        beta = rz_new / rz
+        rz = rz_new
+        for d in range(len(p)):
+            p[d] = z[d] + beta * p[d]
+    return x, max_iters
+
+
+def rebalance(factors) -> None:
+    """optim.py:534-555."""
+    norms = np.stack([np.linalg.norm(f, axis=0) for f in factors])
+    ok = np.all(norms > 0.0, axis=0)
+    if not np.any(ok):
+        return
+    target = np.exp(np.log(norms[:, ok]).mean(axis=0))
+    for n in range(len(factors)):
+        scale = np.ones(norms.shape[1])
+        scale[ok] = target / norms[n, ok]
+        factors[n] *= scale
+
+
+def gn_step(t: OTensor, factors, ident: str, reg: float, cg_tol: float, cg_max: int,
+            variant: str = "gauss_newton", damping_state: dict | None = None,
+            gn_damping: float = 0.0, gn_damping_decay: float = 0.5) -> int:
+    """optim.py:558-598 (in place); returns the CG iterations used."""
+    dphi, d2phi = loss_derivs(ident)
+    model = tttp(t.with_values(np.ones(t.nnz)), factors)
+    phi1 = t.with_values(dphi(t.values, model))
+    phi2 = t.with_values(d2phi(t.values, model))
+    if np.any(phi2.values < 0.0):
+        raise OracleError("negative_curvature")
+    n = t.order
+    grad = [mttkrp(phi1, factors, d) + 2.0 * reg * factors[d] for d in range(n)]
+    grams = [gram_blocks(phi2, factors, d) for d in range(n)]
+    st = damping_state if damping_state is not None else {}
+    if gn_damping > 0.0 and st.get("d") is None:
+        st["d"] = gn_damping * float(np.mean([np.mean(np.diagonal(g, axis1=1, axis2=2))
+                                              for g in grams]))
+    reg_eff = reg + (st.get("d") or 0.0)
+    eye = np.eye(factors[0].shape[1])
+    systems = [g + 2.0 * reg_eff * eye for g in grams]
+
+    def precond(blocks):
+        return [np.linalg.solve(a, b[:, :, None])[:, :, 0] for a, b in zip(systems, blocks)]
+
+    def matvec(x):
+        return hessian_matvec(phi1, phi2, factors, x, variant, reg_eff)
+
+    delta, used = pcg(matvec, precond, [-g for g in grad], cg_tol, cg_max)
+    for d in range(n):
+        factors[d] = factors[d] + delta[d]
+    rebalance(factors)
+    if st.get("d") is not None:
+        st["d"] *= gn_damping_decay
+    return used

@@ -37,7 +37,7 @@ SYMBOLS = (
     "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_update", "cpfit_probe_gather",
     "cpfit_solve_rows", "cpfit_dense_reduce", "cpfit_khatri_rao", "cpfit_als_update",
     "cpfit_ccd_numden", "cpfit_ccd_apply", "cpfit_check_finite",
-    "cpfit_tttp_host",
+    "cpfit_tttp_host", "cpfit_tttp_subst", "cpfit_axpby",
 )
 
 _vp = ctypes.c_void_p
@@ -93,6 +93,8 @@ def load(path: str | None = None):
                              ctypes.POINTER(_int), _vp],
         "cpfit_ccd_update": [_vp, _int, _PP, _vp, _vp, _vp, ctypes.c_double, _vp],
         "cpfit_tttp_host": [_vp, _int, _int, _vp, _PP, _vp, _vp, _i64, _vp],
+        "cpfit_tttp_subst": [_vp, _int, _int, _vp, _PP, _PP, _vp, _vp],
+        "cpfit_axpby": [_int, _i64, ctypes.c_double, _vp, ctypes.c_double, _vp, _vp, _vp],
         "cpfit_check_finite": [_int, _i64, _vp, _vp, _vp],
         "cpfit_ccd_numden": [_vp, _int, _PP, _vp, _vp, _vp, _vp],
         "cpfit_ccd_apply": [_vp, _int, _PP, _vp, _vp, ctypes.c_double, _vp, _vp, _vp],

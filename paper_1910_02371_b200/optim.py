@@ -34,6 +34,8 @@ from .exceptions import NumericalError
 from .kernels import _ptrs, gram_blocks, mttkrp, solve_factor, tttp
 from .losses import (LossFunction, derivative_tensors, factor_sq_norms, get_loss,
                      ls_data_term, model_at_observed, tttp_affine)
+from .second_order import (BlockDiagPreconditioner, gn_step, gradient_blocks,  # noqa: F401
+                           hessian_matvec, pcg_solve, rebalance_factors)
 from .trace import RunTrace
 from .validation import _is_torch
 
@@ -475,10 +477,6 @@ def sgd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
 
 def run(t: SparseTensor, cfg: SolverConfig, return_state: bool = False):
     """Run the configured solver and collect a convergence trace (optim.py:604-691)."""
-    if cfg.algorithm in ("gn", "newton"):
-        raise NotImplementedError(
-            "Gauss-Newton / Newton steps are outside this build's hot-path scope "
-            "(SURVEY.md 8f rank 1)")
     loss = get_loss(cfg.loss)
     loss.validate_data(t.values)
     root = RngState(cfg.seed)
@@ -498,6 +496,9 @@ def run(t: SparseTensor, cfg: SolverConfig, return_state: bool = False):
         state.factors = _to_dev_factors(state.factors)
     mask = t.observation_mask()
     start = time.perf_counter()
+    if cfg.algorithm in ("gn", "newton") and cfg.warmup_sweeps:
+        for _ in range(cfg.warmup_sweeps):
+            als_sweep(t, state, loss, cfg)
 
     def evaluate():
         if ls:
@@ -525,8 +526,12 @@ def run(t: SparseTensor, cfg: SolverConfig, return_state: bool = False):
             als_sweep(t, state, loss, cfg)
         elif cfg.algorithm == "ccd":
             ccd_sweep(t, state, loss, cfg)
-        else:
+        elif cfg.algorithm == "sgd":
             sgd_sweep(t, state, loss, cfg, sgd_rng.child(it))
+        elif cfg.algorithm == "gn":
+            gn_step(t, state, loss, cfg, variant="gauss_newton")
+        else:
+            gn_step(t, state, loss, cfg, variant="newton")
         state.iteration = it
         for d, f in enumerate(state.factors):
             total = float(f.sum()) if _is_torch(f) else float(np.sum(f))

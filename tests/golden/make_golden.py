@@ -19,6 +19,9 @@ Fixtures:
   cfg1.npz           -- BASELINE cfg 1: tttp, mttkrp x3, 5 ALS sweeps (+rmse),
                         2 CCD++ sweeps, 3 SGD steps, all from the reference
   drivers_small.npz  -- ALS/CCD/SGD single sweeps and run() traces, small case
+  second_order.npz   -- hessian_matvec (ls/poisson x gauss_newton/newton),
+                        gradient_blocks, gn_step trajectories (ls GN, ls
+                        Newton, poisson GN) and run(algorithm=gn/newton) traces
 """
 
 from __future__ import annotations
@@ -201,7 +204,95 @@ def drivers_small():
     np.savez_compressed(os.path.join(HERE, "drivers_small.npz"), **out)
 
 
+def second_order():
+    rng = np.random.default_rng(31)
+    out = {}
+    # implicit Hessian products on small fully observed instances
+    case = 0
+    for ident in ("ls", "poisson"):
+        for variant in ("gauss_newton", "newton"):
+            dims = (4, 3, 2) if case % 2 == 0 else (5, 3, 3, 2)
+            total = int(np.prod(dims))
+            keys = np.arange(total, dtype=np.uint64)
+            vals = rng.random(total) * 3.0 if ident == "poisson" else \
+                rng.standard_normal(total)
+            t = cpfit.SparseTensor(dims, keys, vals)
+            factors = [0.5 * rng.standard_normal((d, 2)) for d in dims]
+            x = [rng.standard_normal((d, 2)) for d in dims]
+            loss = cpfit.get_loss(ident)
+            model = cpfit.model_at_observed(t.observation_mask(), factors)
+            phi1, phi2 = cpfit.derivative_tensors(loss, t, model)
+            reg = float(rng.random() * 0.4)
+            y = ro.hessian_matvec(phi1, phi2, factors, x, variant=variant, reg=reg)
+            g = ro.gradient_blocks(t, factors, loss, reg)
+            out[f"hv{case}_dims"] = np.array(dims)
+            out[f"hv{case}_vals"] = vals
+            out[f"hv{case}_ident"] = np.array(ident)
+            out[f"hv{case}_variant"] = np.array(variant)
+            out[f"hv{case}_reg"] = np.array(reg)
+            for n in range(len(dims)):
+                out[f"hv{case}_f{n}"] = factors[n]
+                out[f"hv{case}_x{n}"] = x[n]
+                out[f"hv{case}_y{n}"] = y[n]
+                out[f"hv{case}_g{n}"] = g[n]
+            case += 1
+    out["hv_cases"] = np.array(case)
+    # gn_step trajectories near a low-rank truth
+    t, truth = cpfit.gen_low_rank((24, 20, 16), 3, 0.4, rng=cpfit.RngState(32))
+    noise = np.random.default_rng(33)
+    init = [f + 0.05 * noise.standard_normal(f.shape) for f in truth]
+    out["gn_dims"] = np.array(t.shape)
+    out["gn_keys"] = t.keys
+    out["gn_values"] = t.values
+    for n in range(3):
+        out[f"gn_init{n}"] = init[n]
+    for tag, variant, ident, kw in (("gnls", "gauss_newton", "ls", {}),
+                                    ("ntls", "newton", "ls", {}),
+                                    ("gnls_damped", "gauss_newton", "ls",
+                                     {"gn_damping": 0.1})):
+        cfg = ro.SolverConfig(rank=3, reg=1e-4, cg_tol=1e-10, cg_max=300, **kw)
+        state = ro.CompletionState(factors=[f.copy() for f in init], rng=cpfit.RngState(0))
+        used = []
+        for s in range(3):
+            used.append(ro.gn_step(t, state, cpfit.get_loss(ident), cfg, variant=variant))
+            for n in range(3):
+                out[f"{tag}{s}_f{n}"] = state.factors[n].copy()
+        out[f"{tag}_cg"] = np.array(used)
+    # poisson: counts from the truth model
+    tp = t.with_values(np.round(t.values * 4.0))
+    out["gnpo_values"] = tp.values
+    cfg = ro.SolverConfig(rank=3, reg=1e-3, cg_tol=1e-10, cg_max=300, loss="poisson")
+    pinit = [0.3 * f for f in init]
+    for n in range(3):
+        out[f"gnpo_init{n}"] = pinit[n]
+    state = ro.CompletionState(factors=[f.copy() for f in pinit], rng=cpfit.RngState(0))
+    used = []
+    for s in range(2):
+        used.append(ro.gn_step(tp, state, cpfit.get_loss("poisson"), cfg))
+        for n in range(3):
+            out[f"gnpo{s}_f{n}"] = state.factors[n].copy()
+    out["gnpo_cg"] = np.array(used)
+    # run() traces
+    rng2 = np.random.default_rng(26)
+    ts = random_sparse((8, 7, 6), 0.5, rng2)
+    for algo, kw in (("gn", {"calibrate_init": True, "gn_damping": 1.0}),
+                     ("newton", {"warmup_sweeps": 1, "gn_damping": 1.0, "calibrate_init": True})):
+        cfg = ro.SolverConfig(rank=3, algorithm=algo, max_iters=3, seed=4, deterministic=True,
+                              record_every=1, **kw)
+        trace, state = ro.run(ts, cfg, return_state=True)
+        out[f"run_{algo}_obj"] = np.array([r.objective for r in trace.records])
+        out[f"run_{algo}_metric"] = np.array([r.metric for r in trace.records])
+        out[f"run_{algo}_iters"] = np.array([r.iteration for r in trace.records])
+        for n in range(3):
+            out[f"run_{algo}_f{n}"] = state.factors[n]
+    np.savez_compressed(os.path.join(HERE, "second_order.npz"), **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     kernels_small()
     layout()
     philox()
