@@ -308,6 +308,28 @@ def als_section(world, rank, dev, sweeps=3):
         torch.cuda.synchronize()
         out["ccd_sweep_ms"] = a.elapsed_time(b)
         out["ccd_sweep_cpu_reference_s"] = CPU_CCD_SURVEY_S
+        # one Gauss-Newton step from the ALS iterate
+        from paper_1910_02371_b200.optim import CompletionState, SolverConfig
+        from paper_1910_02371_b200.second_order import gn_step_device
+        from paper_1910_02371_b200.losses import get_loss
+        gcfg = SolverConfig(rank=R3, reg=REG, gn_damping=1.0)
+        st = CompletionState(factors=F, rng=cp.RngState(0))
+        Fg = [f.clone() for f in init]
+        _als_ls_device(t, Fg, REG)
+        gn_step_device(t, Fg, get_loss("ls"), gcfg, st, "gauss_newton")  # warm-up
+        st = CompletionState(factors=F, rng=cp.RngState(0))
+        Fg = [f.clone() for f in init]
+        _als_ls_device(t, Fg, REG)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        cg = gn_step_device(t, Fg, get_loss("ls"), gcfg, st, "gauss_newton")
+        b.record(stream)
+        torch.cuda.synchronize()
+        out["gn_step_ms"] = a.elapsed_time(b)
+        out["gn_step_cg_iters"] = cg
+        out["gn_step_note"] = ("one damped Gauss-Newton step (gn_damping=1, cg_tol 5e-3, "
+                               "cg_max min(30, 3R)) after one ALS sweep from the default init")
     else:
         from paper_1910_02371_b200 import dist as D
         coords = []

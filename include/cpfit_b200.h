@@ -176,6 +176,19 @@ int cpfit_tttp_subst(cpfit_pattern *p, int dtype, int rank, const void *w,
                      const void *const *factors, const void *const *xblocks,
                      void *out, void *stream);
 
+/* Block-diagonal preconditioner of the second-order step (optim.py:467-487),
+ * inverted once per step: inv_out[i] = (gram[i] + shift I)^{-1} for rank <= 32
+ * (warp Gauss-Jordan on the SPD blocks).  *nbad = rows whose pivots were not
+ * positive (then the caller solves that mode with cpfit_solve_rows, whose
+ * LU fallback reports singular systems like np.linalg.solve).  Synchronous. */
+int cpfit_spd_inverse_rows(int dtype, int rank, int64_t nrows, const void *gram,
+                           int64_t gram_stride, double shift, void *inv_out,
+                           int64_t *nbad, void *stream);
+
+/* y[i] = mats[i] x[i] for symmetric rank x rank blocks (rank <= 32). */
+int cpfit_batched_symv(int dtype, int rank, int64_t nrows, const void *mats,
+                       const void *x, void *y, void *stream);
+
 /* out[k] = a * x[k] + b * y[k] (PCG vector updates, optim.py:513-531). */
 int cpfit_axpby(int dtype, int64_t n, double a, const void *x, double b,
                 const void *y, void *out, void *stream);

@@ -37,7 +37,8 @@ SYMBOLS = (
     "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_update", "cpfit_probe_gather",
     "cpfit_solve_rows", "cpfit_dense_reduce", "cpfit_khatri_rao", "cpfit_als_update",
     "cpfit_ccd_numden", "cpfit_ccd_apply", "cpfit_check_finite",
-    "cpfit_tttp_host", "cpfit_tttp_subst", "cpfit_axpby",
+    "cpfit_tttp_host", "cpfit_tttp_subst", "cpfit_axpby", "cpfit_spd_inverse_rows",
+    "cpfit_batched_symv",
 )
 
 _vp = ctypes.c_void_p
@@ -95,6 +96,9 @@ def load(path: str | None = None):
         "cpfit_tttp_host": [_vp, _int, _int, _vp, _PP, _vp, _vp, _i64, _vp],
         "cpfit_tttp_subst": [_vp, _int, _int, _vp, _PP, _PP, _vp, _vp],
         "cpfit_axpby": [_int, _i64, ctypes.c_double, _vp, ctypes.c_double, _vp, _vp, _vp],
+        "cpfit_spd_inverse_rows": [_int, _int, _i64, _vp, _i64, ctypes.c_double, _vp,
+                                   ctypes.POINTER(_i64), _vp],
+        "cpfit_batched_symv": [_int, _int, _i64, _vp, _vp, _vp, _vp],
         "cpfit_check_finite": [_int, _i64, _vp, _vp, _vp],
         "cpfit_ccd_numden": [_vp, _int, _PP, _vp, _vp, _vp, _vp],
         "cpfit_ccd_apply": [_vp, _int, _PP, _vp, _vp, ctypes.c_double, _vp, _vp, _vp],

@@ -154,16 +154,44 @@ class _DeviceOperator:
 
 
 class _DevicePreconditioner:
-    """Inverse of the per-mode diagonal blocks (G_i + shift I), optim.py:467-487."""
+    """Inverse of the per-mode diagonal blocks (G_i + shift I), optim.py:467-487.
+
+    For rank <= 32 the blocks are inverted once, at the first application
+    (``cpfit_spd_inverse_rows``), and every application is a batched
+    symmetric mat-vec; a mode with a non-positive pivot keeps the pivoted
+    solve per application so singular systems raise like np.linalg.solve."""
 
     def __init__(self, grams, shift: float, op: _DeviceOperator):
         self.grams, self.shift, self.op = grams, float(shift), op
+        self.inv = None
+
+    def _invert(self):
+        torch = _torch()
+        rank = self.op.rank
+        self.inv = []
+        for g in self.grams:
+            if rank > 32 or g.shape[0] == 0:
+                self.inv.append(None)
+                continue
+            inv = torch.empty_like(g)
+            nbad = ctypes.c_int64(0)
+            _lib.check(_lib.load().cpfit_spd_inverse_rows(
+                _dtype_code(g.dtype), rank, g.shape[0], _vp(g), rank * rank, self.shift,
+                _vp(inv), ctypes.byref(nbad), _s()), "spd_inverse_rows")
+            self.inv.append(inv if nbad.value == 0 else None)
 
     def __call__(self, rflat):
         torch = _torch()
+        if self.inv is None:
+            self._invert()
         out = torch.empty_like(rflat)
         rank = self.op.rank
         for d, (r, z) in enumerate(zip(self.op.blocks(rflat), self.op.blocks(out))):
+            if self.inv[d] is not None:
+                _lib.check(_lib.load().cpfit_batched_symv(
+                    _dtype_code(r.dtype), rank, r.shape[0], _vp(self.inv[d]), _vp(r), _vp(z),
+                    _s()), "batched_symv")
+                continue
             bad = ctypes.c_int64(-1)
             st = _lib.load().cpfit_solve_rows(_dtype_code(r.dtype), rank, r.shape[0],
                                               _vp(self.grams[d]), rank * rank, _vp(r),

@@ -154,3 +154,17 @@ def test_gn_device_resident_factors():
     assert all(f.is_cuda for f in st.factors)
     for n in range(3):
         assert rel(st.factors[n].cpu().numpy(), z[f"gnls0_f{n}"]) < 1e-8
+
+
+def test_singular_preconditioner_raises():
+    # reg = 0 and a mode-0 row without entries: (G_i + 0 I) = 0 is singular,
+    # like np.linalg.solve in the reference's BlockDiagPreconditioner.apply
+    keys = np.array([k for k in range(4 * 3 * 3)], dtype=np.uint64)
+    t = cp.SparseTensor((5, 3, 3), keys, np.random.default_rng(1).standard_normal(keys.size))
+    fs = [np.random.default_rng(2 + n).standard_normal((d, 2)) for n, d in enumerate(t.shape)]
+    st = CompletionState(factors=fs, rng=cp.RngState(0))
+    with pytest.raises(NumericalError, match="singular block-diagonal preconditioner"):
+        cp.gn_step(t, st, cp.get_loss("ls"), SolverConfig(rank=2, reg=0.0))
+    pre = cp.BlockDiagPreconditioner(t.with_values(np.full(t.nnz, 2.0)), fs, 0.0)
+    with pytest.raises(NumericalError):
+        pre.apply([np.ones_like(f) for f in fs])
