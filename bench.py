@@ -716,29 +716,29 @@ def main():
                        "pinned-host numpy factors uploaded on every call and numpy results "
                        "read back; t persistent (values uploaded once, pattern cached)"}
 
+    # sections: SGD (cfg 5, the largest footprint) first, on a clean pool
+    del t, tout, mouts, svals, vals
+    torch.cuda.empty_cache()
+    sgd = None
+    if not args.no_sgd:
+        try:
+            sgd = sgd_section(dev, world=world)
+        except Exception as exc:  # reported, never fatal to the headline line
+            sgd = {"error": repr(exc)}
+        torch.cuda.empty_cache()
     als = None
     if not args.no_als:
-        del t, tout, mouts, svals, vals
-        torch.cuda.empty_cache()
         try:
             als = als_section(world, rank, dev)
-        except Exception as exc:  # reported, never fatal to the headline line
+        except Exception as exc:
             als = {"error": repr(exc)}
+        torch.cuda.empty_cache()
     dense = None
     if not args.no_dense and world == 1:
-        torch.cuda.empty_cache()
         try:
             dense = dense_section(dev)
         except Exception as exc:
             dense = {"error": repr(exc)}
-    sgd = None
-    if not args.no_sgd:
-        torch.cuda.empty_cache()
-        try:
-            sgd = sgd_section(dev, world=world)
-        except Exception as exc:
-            sgd = {"error": repr(exc)}
-        torch.cuda.empty_cache()
 
     if rank == 0:
         line = {
