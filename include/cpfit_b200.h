@@ -229,28 +229,34 @@ int cpfit_sgd_update(int dtype, int64_t n, const void *a, const void *grad,
                      double step, double shrink, void *out, int *nonfinite,
                      void *stream);
 
-/* One CCD++ column update of `mode` for rank-one column r (least squares,
- * optim.py:249-268).  cols[q] = column r of factor q (contiguous, fp64);
- * cols[mode] is ignored and `old_col` used instead; the updated column is
- * written to new_col and the canonical-order residual updated in place. */
-int cpfit_ccd_update(cpfit_pattern *p, int mode, const double *const *cols,
-                     const double *old_col, double *new_col, double *resid,
-                     double reg, void *stream);
-
-/* Distributed CCD++ (nonzeros sharded, one all-reduce per
- * (r, mode)).  cpfit_ccd_numden writes this shard's per-row sums
- * numden[i] = sum rho_e partial_e, numden[I_n + i] = sum partial_e^2
- * (2 * dims[mode] doubles, zero for rows without local entries);
- * after the caller sums numden over ranks, cpfit_ccd_apply computes
- * new_col[i] = num / (den + reg) (old_col[i] when den + reg <= 0) and
- * updates the residual of the local entries.  On one rank the pair equals
- * cpfit_ccd_update bit for bit. */
-int cpfit_ccd_numden(cpfit_pattern *p, int mode, const double *const *cols,
-                     const double *old_col, const double *resid, double *numden,
-                     void *stream);
-int cpfit_ccd_apply(cpfit_pattern *p, int mode, const double *const *cols,
-                    const double *old_col, const double *numden, double reg,
-                    double *new_col, double *resid, void *stream);
+/* CCD++ (least squares, optim.py:235-268 column-then-mode order).  The
+ * device keeps rhat = the residual with the current rank-one column r added
+ * back (canonical entry order, fp64): in exact arithmetic it is the `rho` of
+ * every mode update of column r (optim.py:254), so no per-mode residual pass
+ * is needed.  A sweep is, per column r:
+ *   cpfit_ccd_step(mode 0, fold=1, fold_sub = column r-1 or NULL)   -- rhat of r
+ *   cpfit_ccd_step(mode 1..N-1, fold=0)
+ * and after the last column cpfit_ccd_fold(sub = column R-1, add = NULL),
+ * which leaves the residual t - model in rhat.  Start with rhat = t - model.
+ *
+ * cpfit_ccd_step: cols[q] = column r of factor q (contiguous fp64, length
+ * dims[q]).  fold != 0 (identity-order mode 0 only): rhat is first replaced
+ * by (rhat - prod fold_sub) + prod cols over every entry and written back.
+ * numden == NULL: cols[mode] is updated in place, new_i = num_i / (den_i +
+ * reg), the old value kept where den_i + reg <= 0 (optim.py:260-263), with
+ * num_i = sum rhat_e partial_e, den_i = sum partial_e^2 over row i.
+ * numden != NULL (distributed: nonzeros sharded, one all-reduce
+ * per (r, mode)): writes numden[i] = num_i, numden[dims[mode] + i] = den_i
+ * (zero for rows without local entries) and leaves cols untouched; after
+ * the caller sums numden over ranks, cpfit_ccd_finalize applies the update
+ * rule to the column.  One rank reproduces the fused path bit for bit. */
+int cpfit_ccd_step(cpfit_pattern *p, int mode, double *const *cols, double *rhat,
+                   int fold, const double *const *fold_sub, double reg,
+                   double *numden, void *stream);
+int cpfit_ccd_fold(cpfit_pattern *p, const double *const *sub,
+                   const double *const *add, double *rhat, void *stream);
+int cpfit_ccd_finalize(int64_t dim, const double *numden, double reg,
+                       double *col, void *stream);
 
 /* Batched regularised SPD solves without a tensor pattern:
  * (G_i + reg I) x_i = rhs_i for i < nrows, G_i = gram + i * gram_stride

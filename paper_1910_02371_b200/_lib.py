@@ -34,9 +34,9 @@ SYMBOLS = (
     "cpfit_pattern_mode_group", "cpfit_pattern_mode_stats", "cpfit_permute_values",
     "cpfit_tttp", "cpfit_mttkrp", "cpfit_gram", "cpfit_solve_factor",
     "cpfit_tttp_axpby", "cpfit_sample", "cpfit_pattern_parent_index", "cpfit_gather_values",
-    "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_update", "cpfit_probe_gather",
+    "cpfit_reduce", "cpfit_sgd_update", "cpfit_ccd_step", "cpfit_probe_gather",
     "cpfit_solve_rows", "cpfit_dense_reduce", "cpfit_khatri_rao", "cpfit_als_update",
-    "cpfit_ccd_numden", "cpfit_ccd_apply", "cpfit_check_finite",
+    "cpfit_ccd_fold", "cpfit_ccd_finalize", "cpfit_check_finite",
     "cpfit_tttp_host", "cpfit_tttp_subst", "cpfit_axpby", "cpfit_spd_inverse_rows",
     "cpfit_batched_symv",
 )
@@ -92,7 +92,7 @@ def load(path: str | None = None):
         "cpfit_reduce": [_int, _int, _i64, _vp, _vp, ctypes.POINTER(ctypes.c_double), _vp],
         "cpfit_sgd_update": [_int, _i64, _vp, _vp, ctypes.c_double, ctypes.c_double, _vp,
                              ctypes.POINTER(_int), _vp],
-        "cpfit_ccd_update": [_vp, _int, _PP, _vp, _vp, _vp, ctypes.c_double, _vp],
+        "cpfit_ccd_step": [_vp, _int, _PP, _vp, _int, _PP, ctypes.c_double, _vp, _vp],
         "cpfit_tttp_host": [_vp, _int, _int, _vp, _PP, _vp, _vp, _i64, _vp],
         "cpfit_tttp_subst": [_vp, _int, _int, _vp, _PP, _PP, _vp, _vp],
         "cpfit_axpby": [_int, _i64, ctypes.c_double, _vp, ctypes.c_double, _vp, _vp, _vp],
@@ -100,8 +100,8 @@ def load(path: str | None = None):
                                    ctypes.POINTER(_i64), _vp],
         "cpfit_batched_symv": [_int, _int, _i64, _vp, _vp, _vp, _vp],
         "cpfit_check_finite": [_int, _i64, _vp, _vp, _vp],
-        "cpfit_ccd_numden": [_vp, _int, _PP, _vp, _vp, _vp, _vp],
-        "cpfit_ccd_apply": [_vp, _int, _PP, _vp, _vp, ctypes.c_double, _vp, _vp, _vp],
+        "cpfit_ccd_fold": [_vp, _PP, _PP, _vp, _vp],
+        "cpfit_ccd_finalize": [_i64, _vp, ctypes.c_double, _vp, _vp],
         "cpfit_probe_gather": [_vp, _int, _int, _PP, _i64, _vp, _i64, _vp],
         "cpfit_solve_rows": [_int, _int, _i64, _vp, _i64, _vp, ctypes.c_double, _vp,
                              ctypes.POINTER(_i64), _vp],

@@ -138,8 +138,9 @@ class ShardedCCD:
     """Nonzero-sharded CCD++ sweeps: each rank keeps a
     contiguous key range of the entries and its slice of the residual; per
     (r, mode) the per-row (num, den) sums of the shard are all-reduced (2 I_n
-    values) and every rank computes the identical new column, then updates
-    its local residual.  optim.py:235-268 least-squares branch.
+    values) and every rank computes the identical new column; the shard's
+    rhat (residual with column r added back) is re-formed once per column.
+    optim.py:235-268 least-squares branch.
 
     backend: ccd_begin(shard, factors) -> state; ccd_numden(shard, state, r,
     mode) -> comm tensor (2 I_n); ccd_apply(shard, state, r, mode, numden, reg);
@@ -226,36 +227,39 @@ class DeviceBackend:
         from .core import SparseTensor
         return SparseTensor.from_device(shape, keys.contiguous(), values.contiguous())
 
-    # -- CCD++ (cpfit_ccd_numden / cpfit_ccd_apply) --
+    # -- CCD++ (cpfit_ccd_step with numden / cpfit_ccd_finalize / cpfit_ccd_fold) --
     def ccd_begin(self, shard, factors):
         torch = self.torch
         from .losses import tttp_affine
         cols = [f.t().contiguous() for f in factors]  # R x I_n
-        resid = tttp_affine(shard, factors, -1.0, 1.0, torch.float64)
-        tmp = [torch.empty(d, dtype=torch.float64, device=factors[0].device)
-               for d in shard.shape]
-        return {"cols": cols, "resid": resid, "tmp": tmp}
+        rhat = tttp_affine(shard, factors, -1.0, 1.0, torch.float64)  # t - model
+        return {"cols": cols, "rhat": rhat, "prev": None, "shard": shard}
 
     def _ccd_ptrs(self, state, r):
         import ctypes
 
         from . import _lib
-        cp = [c[r] for c in state["cols"]]
-        arr = _lib.ptr_array([c.data_ptr() for c in cp])
-        return cp, arr, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
+        arr = _lib.ptr_array([c[r].data_ptr() for c in state["cols"]])
+        return arr, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
 
     def ccd_numden(self, shard, state, r, mode):
+        """Local (num, den) of column r on `mode`; mode 0 first re-forms the
+        shard's rhat for column r (fused fold, csrc/ccd.cu)."""
         import ctypes
 
         from . import _lib
         from .optim import _stream
-        cp, _keep, ptrs = self._ccd_ptrs(state, r)
+        keep, ptrs = self._ccd_ptrs(state, r)
+        state["cur"] = (keep, ptrs)
         nd = self.torch.empty(2 * shard.shape[mode], dtype=self.torch.float64,
-                              device=cp[0].device)
-        _lib.check(_lib.load().cpfit_ccd_numden(
-            shard.device_pattern().handle, mode, ptrs, ctypes.c_void_p(cp[mode].data_ptr()),
-            ctypes.c_void_p(state["resid"].data_ptr()), ctypes.c_void_p(nd.data_ptr()),
-            _stream()), "ccd_numden")
+                              device=state["rhat"].device)
+        sub = state["prev"][1] if (mode == 0 and state["prev"] is not None) else None
+        _lib.check(_lib.load().cpfit_ccd_step(
+            shard.device_pattern().handle, mode, ptrs,
+            ctypes.c_void_p(state["rhat"].data_ptr()), 1 if mode == 0 else 0, sub, 0.0,
+            ctypes.c_void_p(nd.data_ptr()), _stream()), "ccd_step")
+        if mode == 0:
+            state["prev"] = None
         return nd
 
     def ccd_apply(self, shard, state, r, mode, nd, reg):
@@ -263,15 +267,22 @@ class DeviceBackend:
 
         from . import _lib
         from .optim import _stream
-        cp, _keep, ptrs = self._ccd_ptrs(state, r)
-        tmp = state["tmp"][mode]
-        _lib.check(_lib.load().cpfit_ccd_apply(
-            shard.device_pattern().handle, mode, ptrs, ctypes.c_void_p(cp[mode].data_ptr()),
-            ctypes.c_void_p(nd.data_ptr()), float(reg), ctypes.c_void_p(tmp.data_ptr()),
-            ctypes.c_void_p(state["resid"].data_ptr()), _stream()), "ccd_apply")
-        cp[mode].copy_(tmp)
+        col = state["cols"][mode][r]
+        _lib.check(_lib.load().cpfit_ccd_finalize(
+            col.numel(), ctypes.c_void_p(nd.data_ptr()), float(reg),
+            ctypes.c_void_p(col.data_ptr()), _stream()), "ccd_finalize")
+        if mode == shard.order - 1:
+            state["prev"] = state["cur"]
 
     def ccd_end(self, state, factors):
+        import ctypes
+
+        from . import _lib
+        from .optim import _stream
+        if state["prev"] is not None and state["rhat"].numel():
+            _lib.check(_lib.load().cpfit_ccd_fold(
+                state["shard"].device_pattern().handle, state["prev"][1], None,
+                ctypes.c_void_p(state["rhat"].data_ptr()), _stream()), "ccd_fold")
         for n, c in enumerate(state["cols"]):
             factors[n] = c.t().contiguous()
 

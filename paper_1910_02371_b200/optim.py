@@ -8,8 +8,9 @@ the device end to end:
 * ALS (optim.py:180-207): per mode, MTTKRP of the data (rhs) and the fused
   Gram assembly + batched SPD solve with unit weights (the observation mask is
   never materialised); reg, not 2 reg, on the diagonal.
-* CCD++ (optim.py:235-268): the residual lives on the device; each (r, mode)
-  step is one segmented num/den pass plus one residual pass.
+* CCD++ (optim.py:235-268): the residual lives on the device as rhat (the
+  residual with column r added back, every mode's rho); each (r, mode) step
+  is one segmented num/den pass, and rhat is re-formed once per column.
 * SGD (optim.py:300-330): bit-exact device Philox sample, derivative tensor
   2(m - t) fused into TTTP, sampled MTTKRPs at the pre-step factors, update
   in numpy's evaluation order.
@@ -319,29 +320,42 @@ def _like(ref, a):
 # ---------------------------------------------------------------------------
 # coordinate minimization
 
+def _ccd_col_ptrs(cols, r):
+    """Pointer array to column r of every mode (cols[n] is R x I_n)."""
+    arr = _lib.ptr_array([c[r].data_ptr() for c in cols])
+    return arr, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
+
+
 def _ccd_ls_device(t: SparseTensor, F, reg: float):
-    """CCD++ least-squares sweep on device factors (list of f64 CUDA tensors)."""
+    """CCD++ least-squares sweep on device factors (list of f64 CUDA tensors).
+
+    Column r keeps rhat = resid + (rank-one term of column r) on the device:
+    it is every mode's rho of the reference (optim.py:254) in exact
+    arithmetic, so each (r, mode) update is one segmented (num, den) pass and
+    the residual is re-formed once per column, fused into the mode-0 pass
+    (csrc/ccd.cu).  Returns the residual t - model."""
     torch = _torch()
     order = t.order
     rank = F[0].shape[1]
     L = _lib.load()
     pat = t.device_pattern()
     cols = [f.t().contiguous() for f in F]  # R x I_n: column r contiguous
-    resid = tttp_affine(t, F, -1.0, 1.0, torch.float64)  # t - model
-    tmp = [torch.empty(t.shape[n], dtype=torch.float64, device=F[0].device)
-           for n in range(order)]
+    rhat = tttp_affine(t, F, -1.0, 1.0, torch.float64)  # t - model
+    prev = None
     for r in range(rank):
-        cp = [cols[n][r] for n in range(order)]
-        ptrs = _lib.ptr_array([c.data_ptr() for c in cp])
+        keep, ptrs = _ccd_col_ptrs(cols, r)
         for mode in range(order):
-            _lib.check(L.cpfit_ccd_update(
-                pat.handle, mode, ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)),
-                ctypes.c_void_p(cp[mode].data_ptr()), ctypes.c_void_p(tmp[mode].data_ptr()),
-                ctypes.c_void_p(resid.data_ptr()), float(reg), _stream()), "ccd_update")
-            cp[mode].copy_(tmp[mode])
+            sub = prev[1] if (mode == 0 and prev is not None) else None
+            _lib.check(L.cpfit_ccd_step(pat.handle, mode, ptrs, ctypes.c_void_p(rhat.data_ptr()),
+                                        1 if mode == 0 else 0, sub, float(reg), None, _stream()),
+                       "ccd_step")
+        prev = (keep, ptrs)
+    if prev is not None:
+        _lib.check(L.cpfit_ccd_fold(pat.handle, prev[1], None, ctypes.c_void_p(rhat.data_ptr()),
+                                    _stream()), "ccd_fold")
     for n in range(order):
         F[n] = cols[n].t().contiguous()
-    return resid
+    return rhat
 
 
 def ccd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
