@@ -231,17 +231,22 @@ int cpfit_sgd_update(int dtype, int64_t n, const void *a, const void *grad,
 
 /* CCD++ (least squares, optim.py:235-268 column-then-mode order).  The
  * device keeps rhat = the residual with the current rank-one column r added
- * back (canonical entry order, fp64): in exact arithmetic it is the `rho` of
- * every mode update of column r (optim.py:254), so no per-mode residual pass
- * is needed.  A sweep is, per column r:
- *   cpfit_ccd_step(mode 0, fold=1, fold_sub = column r-1 or NULL)   -- rhat of r
- *   cpfit_ccd_step(mode 1..N-1, fold=0)
- * and after the last column cpfit_ccd_fold(sub = column R-1, add = NULL),
- * which leaves the residual t - model in rhat.  Start with rhat = t - model.
+ * back: in exact arithmetic it is the `rho` of every mode update of column r
+ * (optim.py:254), so no per-mode residual pass is needed.  Each mode n keeps
+ * its own copy rhat_n in its mode-sorted order (mode 0: canonical order);
+ * start with rhat_n = (t - model) permuted (cpfit_permute_values).  A sweep
+ * is, per column r, for n = 0..N-1:
+ *   cpfit_ccd_step(n, rhat_n, rhat_sorted = 1, fold_sub = new column r-1
+ *                  (NULL for r = 0), fold_add = column r as it was before
+ *                  this sweep touched it)
+ * and after the last column cpfit_ccd_fold(mode 0, sub = column R-1, add =
+ * NULL) on rhat_0 leaves the residual t - model in canonical order.
  *
  * cpfit_ccd_step: cols[q] = column r of factor q (contiguous fp64, length
- * dims[q]).  fold != 0 (identity-order mode 0 only): rhat is first replaced
- * by (rhat - prod fold_sub) + prod cols over every entry and written back.
+ * dims[q]).  With fold_sub / fold_add, rhat is first replaced by
+ * (rhat - prod fold_sub) + prod fold_add at every entry (needs rhat_sorted
+ * or an identity-order mode) and written back.  rhat_sorted = 0: a
+ * canonical rhat read through the mode permutation, not folded.
  * numden == NULL: cols[mode] is updated in place, new_i = num_i / (den_i +
  * reg), the old value kept where den_i + reg <= 0 (optim.py:260-263), with
  * num_i = sum rhat_e partial_e, den_i = sum partial_e^2 over row i.
@@ -249,11 +254,14 @@ int cpfit_sgd_update(int dtype, int64_t n, const void *a, const void *grad,
  * per (r, mode)): writes numden[i] = num_i, numden[dims[mode] + i] = den_i
  * (zero for rows without local entries) and leaves cols untouched; after
  * the caller sums numden over ranks, cpfit_ccd_finalize applies the update
- * rule to the column.  One rank reproduces the fused path bit for bit. */
+ * rule to the column.  One rank reproduces the fused path bit for bit.
+ * cpfit_ccd_fold: the fold alone on a copy in mode `mode`'s sorted order
+ * (mode = -1: canonical order). */
 int cpfit_ccd_step(cpfit_pattern *p, int mode, double *const *cols, double *rhat,
-                   int fold, const double *const *fold_sub, double reg,
-                   double *numden, void *stream);
-int cpfit_ccd_fold(cpfit_pattern *p, const double *const *sub,
+                   int rhat_sorted, const double *const *fold_sub,
+                   const double *const *fold_add, double reg, double *numden,
+                   void *stream);
+int cpfit_ccd_fold(cpfit_pattern *p, int mode, const double *const *sub,
                    const double *const *add, double *rhat, void *stream);
 int cpfit_ccd_finalize(int64_t dim, const double *numden, double reg,
                        double *col, void *stream);

@@ -92,7 +92,7 @@ def load(path: str | None = None):
         "cpfit_reduce": [_int, _int, _i64, _vp, _vp, ctypes.POINTER(ctypes.c_double), _vp],
         "cpfit_sgd_update": [_int, _i64, _vp, _vp, ctypes.c_double, ctypes.c_double, _vp,
                              ctypes.POINTER(_int), _vp],
-        "cpfit_ccd_step": [_vp, _int, _PP, _vp, _int, _PP, ctypes.c_double, _vp, _vp],
+        "cpfit_ccd_step": [_vp, _int, _PP, _vp, _int, _PP, _PP, ctypes.c_double, _vp, _vp],
         "cpfit_tttp_host": [_vp, _int, _int, _vp, _PP, _vp, _vp, _i64, _vp],
         "cpfit_tttp_subst": [_vp, _int, _int, _vp, _PP, _PP, _vp, _vp],
         "cpfit_axpby": [_int, _i64, ctypes.c_double, _vp, ctypes.c_double, _vp, _vp, _vp],
@@ -100,7 +100,7 @@ def load(path: str | None = None):
                                    ctypes.POINTER(_i64), _vp],
         "cpfit_batched_symv": [_int, _int, _i64, _vp, _vp, _vp, _vp],
         "cpfit_check_finite": [_int, _i64, _vp, _vp, _vp],
-        "cpfit_ccd_fold": [_vp, _PP, _PP, _vp, _vp],
+        "cpfit_ccd_fold": [_vp, _int, _PP, _PP, _vp, _vp],
         "cpfit_ccd_finalize": [_i64, _vp, ctypes.c_double, _vp, _vp],
         "cpfit_probe_gather": [_vp, _int, _int, _PP, _i64, _vp, _i64, _vp],
         "cpfit_solve_rows": [_int, _int, _i64, _vp, _i64, _vp, ctypes.c_double, _vp,

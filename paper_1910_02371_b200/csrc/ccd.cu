@@ -9,18 +9,23 @@
 // Within one column r, rho is the same tensor for every mode in exact
 // arithmetic: rho_{n+1} = rho_n - partial_n new_n + partial_{n+1} old_{n+1},
 // and both products are the rank-one term with the current columns.  So the
-// device keeps rho itself ("rhat", the residual with column r added back, in
-// canonical entry order) for the whole column and skips the per-mode residual
-// pass: per (r, mode) one segmented pass computes (num, den); between columns
-// one pass folds rhat_{r+1} = (rhat_r - prod new_r) + prod col_{r+1}, fused
-// into the mode-0 pass of column r+1 (mode 0 is in canonical order).  The two
-// products use the reference's multiplication orders at those points (sub:
-// ascending modes, as for the last mode; add: partial over p != 0, then col_0),
-// so only the intermediate rho values differ from the reference, by rounding.
+// device keeps rho itself ("rhat", the residual with column r added back) for
+// the whole column and skips the per-mode residual pass.  Each mode keeps its
+// own copy of rhat in its mode-sorted order, so every pass streams it
+// coalesced instead of gathering 8 B through the permutation (a 64 B DRAM
+// access each on a 0.8 GB array at cfg 3), and each copy is re-formed in its
+// own pass at the start of a column: rhat_r = (rhat_{r-1} - prod new_{r-1}) +
+// prod old_r, with old_r saved before the sweep touches column r.  The
+// products use the reference's multiplication orders (sub: modes ascending,
+// as for the last mode; add: partial over p != 0, then col_0) and the same
+// operands in every copy, so the copies stay bitwise identical; only the
+// intermediate rho values differ from the reference's, by rounding.
 //
-// Pass layout: warp per task of the mode-sorted task table (no atomics, fixed
-// summation order); split rows leave (num, den) partials combined in task
-// order.  Modes other than 0 read rhat through the mode permutation.
+// Pass layout: the flat segmented pass (fixed chunks of the mode-sorted
+// entries per warp, segmented warp scans, chunk-boundary partials combined in
+// chunk order: no atomics, deterministic).  A canonical-only rhat read
+// through the permutation (rhat_sorted = 0) remains available for memory-lean
+// callers; orders beyond 5 use the task-table pass.
 #include <cstring>
 
 #include "common.cuh"
@@ -31,7 +36,8 @@ struct CcdParams {
   int order, mode;
   int64_t nnz, dim;
   double *cols[CPFIT_MAXN];          // column r of every mode (cols[mode] updated in place)
-  const double *sub[CPFIT_MAXN];     // fold: previous column (nullable as a whole)
+  const double *sub[CPFIT_MAXN];     // fold: previous column, new values (nullable as a whole)
+  const double *add[CPFIT_MAXN];     // fold: this column before the sweep touched it (nullable)
   const int32_t *sidx[CPFIT_MAXN];   // mode-sorted coordinates (all modes)
   const int32_t *coords[CPFIT_MAXN];
   const int32_t *perm;               // sorted position -> entry (null: identity)
@@ -42,7 +48,7 @@ struct CcdParams {
   double *slots;                     // 2 * nslots (num, den)
   double *rhat;
   double reg;
-  int fold, has_sub;
+  int fold, has_sub, has_add;
   double *numden;  // non-null: emit (num, den) per row, [num(I_n), den(I_n)], cols untouched
 };
 
@@ -57,9 +63,9 @@ __device__ __forceinline__ double ccd_partial_sorted(const CcdParams &p, int64_t
   return part;
 }
 
-// Pass A: warp per task, U entries per lane in flight.  FOLD (mode 0,
-// identity order): rhat is first rebuilt for this column and written back.
-template <bool FOLD>
+// Task-table pass (orders beyond the flat kernel's instantiations): warp per
+// task, U entries per lane in flight; rhat read at the sorted position (a
+// sorted copy) or through the permutation (canonical rhat).
 __global__ void __launch_bounds__(256) ccd_rows_kernel(const CcdParams p) {
   constexpr int U = 4;
   const int lane = threadIdx.x & 31;
@@ -69,7 +75,6 @@ __global__ void __launch_bounds__(256) ccd_rows_kernel(const CcdParams p) {
     const int64_t b0 = p.task_begin[t], b1 = p.task_begin[t + 1];
     const int64_t row = p.task_row[t];
     const double oc = p.cols[p.mode][row];
-    const double s0 = (FOLD && p.has_sub) ? p.sub[0][row] : 0.0;
     double num = 0.0, den = 0.0;
     for (int64_t e0 = b0 + lane; e0 < b1; e0 += 32 * U) {
       double part[U], rh[U];
@@ -80,36 +85,13 @@ __global__ void __launch_bounds__(256) ccd_rows_kernel(const CcdParams p) {
         rh[u] = 0.0;
         if (e < b1) {
           part[u] = ccd_partial_sorted(p, e);
-          if constexpr (FOLD) {
-            rh[u] = p.rhat[e];
-          } else {
-            const int64_t ent = p.perm ? __ldg(p.perm + e) : e;
-            rh[u] = __ldg(p.rhat + ent);
-          }
+          rh[u] = __ldg(p.rhat + (p.perm ? __ldg(p.perm + e) : e));
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t e = e0 + 32 * u;
-        if (e < b1) {
-          if constexpr (FOLD) {
-            double r = rh[u];
-            if (p.has_sub) {
-              double s = s0;
-#pragma unroll
-              for (int q = 1; q < CPFIT_MAXN; ++q) {
-                if (q >= p.order) break;
-                s = __dmul_rn(s, __ldg(p.sub[q] + __ldg(p.sidx[q] + e)));
-              }
-              r = __dsub_rn(r, s);
-            }
-            r = __dadd_rn(r, __dmul_rn(part[u], oc));
-            p.rhat[e] = r;
-            rh[u] = r;
-          }
-          num += __dmul_rn(rh[u], part[u]);
-          den += __dmul_rn(part[u], part[u]);
-        }
+        num += __dmul_rn(rh[u], part[u]);
+        den += __dmul_rn(part[u], part[u]);
       }
     }
 #pragma unroll
@@ -179,9 +161,10 @@ __global__ void ccd_empty_rows(int64_t dim, const int64_t *__restrict__ offsets,
     if (offsets[i + 1] == offsets[i]) col[i] = 0.0 / reg;
 }
 
-// Canonical-order fold: rhat = (rhat - prod sub) + prod add (either side
-// optional), products in the reference's orders (see the file comment).
-__global__ void ccd_fold_kernel(int order, int64_t nnz, const CcdParams p, int has_add) {
+// Elementwise fold of one rhat copy: rhat = (rhat - prod sub) + prod add
+// (either side optional), products in the reference's orders (see the file
+// comment); p.coords = the copy's coordinate arrays (canonical or sorted).
+__global__ void ccd_fold_kernel(int order, int64_t nnz, const CcdParams p) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
        e += (int64_t)gridDim.x * blockDim.x) {
     int32_t ix[CPFIT_MAXN];
@@ -198,14 +181,14 @@ __global__ void ccd_fold_kernel(int order, int64_t nnz, const CcdParams p, int h
       }
       r = __dsub_rn(r, s);
     }
-    if (has_add) {
+    if (p.has_add) {
       double a = 1.0;
 #pragma unroll
       for (int q = 1; q < CPFIT_MAXN; ++q) {
         if (q >= order) break;
-        a = __dmul_rn(a, __ldg(p.cols[q] + ix[q]));
+        a = __dmul_rn(a, __ldg(p.add[q] + ix[q]));
       }
-      r = __dadd_rn(r, __dmul_rn(a, __ldg(p.cols[0] + ix[0])));
+      r = __dadd_rn(r, __dmul_rn(a, __ldg(p.add[0] + ix[0])));
     }
     p.rhat[e] = r;
   }
@@ -219,7 +202,7 @@ __global__ void ccd_fold_kernel(int order, int64_t nnz, const CcdParams p, int h
 // step sum, carried across steps in entry order.  Rows wholly inside the chunk
 // are finalised by the warp; a row that starts before the chunk leaves its
 // partial in pf[c], one that continues past it in pl[c]; ccd_flat_fixup sums
-// those in chunk order.  FOLD (identity order, mode 0): rhat re-formed first.
+// those in chunk order.  FOLD: this mode's rhat copy is re-formed first.
 #ifndef CCD_FLAT_U
 #define CCD_FLAT_U 2
 #endif
@@ -284,7 +267,6 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int32_t *__restrict__ key = p.sidx[p.mode];
-  const double *__restrict__ mycol = p.cols[p.mode];
   const int mode = p.mode;
   int64_t c = warp;
   int bi = 0;
@@ -314,19 +296,21 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
     }
     CcdBatch<NO, U> nxt;
     if (nc < nchunks) ccd_load_batch<NO, U, FOLD>(p, nc, nb, lane, nxt);
-    // gathers (factor columns, rhat through the permutation)
-    double g[U][NO], sv[U][NO], own[U], rh[U];
+    // gathers (factor columns; rhat through the permutation unless FOLD)
+    double g[U][NO], sv[U][NO], av[U][NO], rh[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      const int32_t rw = cur.row[u] >= 0 ? cur.row[u] : 0;
 #pragma unroll
       for (int q = 0; q < NO; ++q) {
-        g[u][q] = q != mode ? __ldg(p.cols[q] + cur.ix[u][q]) : 1.0;
-        if constexpr (FOLD)
-          sv[u][q] = (p.has_sub && q != mode) ? __ldg(p.sub[q] + cur.ix[u][q]) : 1.0;
+        const int32_t iq = q == mode ? rw : cur.ix[u][q];
+        g[u][q] = q != mode ? __ldg(p.cols[q] + iq) : 1.0;
+        if constexpr (FOLD) {
+          sv[u][q] = p.has_sub ? __ldg(p.sub[q] + iq) : 0.0;
+          av[u][q] = p.has_add ? __ldg(p.add[q] + iq) : 0.0;
+        }
       }
       if constexpr (FOLD) {
-        own[u] = cur.row[u] >= 0 ? mycol[cur.row[u]] : 0.0;
-        if (p.has_sub) sv[u][0] = cur.row[u] >= 0 ? __ldg(p.sub[0] + cur.row[u]) : 0.0;
         rh[u] = cur.rh[u];
       } else {
         rh[u] = cur.row[u] >= 0 ? __ldg(p.rhat + cur.pe[u]) : 0.0;
@@ -340,7 +324,10 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
 #pragma unroll
       for (int q = 0; q < NO; ++q)
         if (q != mode) part = __dmul_rn(part, g[u][q]);
-      if constexpr (FOLD) {  // mode 0
+      if constexpr (FOLD) {
+        // rhat of this column: (rhat - prod sub) + prod add, the products in
+        // the reference's orders (sub: modes ascending; add: partial over
+        // p != 0, then col_0) -- identical in every mode's copy
         double r = rh[u];
         if (p.has_sub) {
           double sp = sv[u][0];
@@ -348,7 +335,12 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
           for (int q = 1; q < NO; ++q) sp = __dmul_rn(sp, sv[u][q]);
           r = __dsub_rn(r, sp);
         }
-        r = __dadd_rn(r, __dmul_rn(part, own[u]));
+        if (p.has_add) {
+          double ap = 1.0;
+#pragma unroll
+          for (int q = 1; q < NO; ++q) ap = __dmul_rn(ap, av[u][q]);
+          r = __dadd_rn(r, __dmul_rn(ap, av[u][0]));
+        }
         const int64_t e = c0 + (int64_t)bi * 32 * U + 32 * u + lane;
         if (cur.row[u] >= 0) p.rhat[e] = r;
         rh[u] = r;
@@ -436,107 +428,6 @@ __global__ void ccd_flat_fixup(const CcdParams p, const int64_t *__restrict__ of
   }
 }
 
-// ---------------------------------------------------------------------------
-// Privatised canonical pass for modes with few rows (dims[mode] * 16 B per
-// warp fits shared memory): entries read in canonical order (coalesced rhat,
-// no permutation), every warp accumulates (num, den) into its own
-// shared-memory row array -- lanes of a step that hit the same row add in
-// lane order, one rank per round (match_any), so the order is fixed -- then the
-// CTA sums its warps in order into cta_part[block], and ccd_priv_finish sums
-// the CTAs in order.  Deterministic, no atomics.
-constexpr int CCD_PRIV_U = 16;
-
-template <int NO, int MODE>
-__global__ void __launch_bounds__(256) ccd_priv_kernel(const CcdParams p, int64_t per_cta,
-                                                       double2 *__restrict__ cta_part) {
-  extern __shared__ double2 acc[];  // [warps][dim]
-  constexpr int U = CCD_PRIV_U;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  const int64_t dim = p.dim;
-  for (int64_t k = threadIdx.x; k < (int64_t)nw * dim; k += blockDim.x)
-    acc[k] = make_double2(0.0, 0.0);
-  __syncthreads();
-  double2 *my = acc + (int64_t)wid * dim;
-  const int64_t b0 = (int64_t)blockIdx.x * per_cta;
-  const int64_t b1 = min(b0 + per_cta, p.nnz);
-  const unsigned lt = (1u << lane) - 1u;
-  for (int64_t base = b0 + (int64_t)wid * 32 * U; base < b1; base += (int64_t)nw * 32 * U) {
-    int32_t row[U];
-    double w1[U], w2[U];
-    int32_t ix[U][NO];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = base + 32 * u + lane;
-#pragma unroll
-      for (int q = 0; q < NO; ++q) ix[u][q] = e < b1 ? __ldg(p.coords[q] + e) : 0;
-      w1[u] = e < b1 ? __ldg(p.rhat + e) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t e = base + 32 * u + lane;
-      double part = 1.0;
-      int32_t r = -1;
-#pragma unroll
-      for (int q = 0; q < NO; ++q) {
-        if (q == MODE) {
-          r = ix[u][q];
-        } else {
-          part = __dmul_rn(part, __ldg(p.cols[q] + ix[u][q]));
-        }
-      }
-      row[u] = e < b1 ? r : -1 - lane;  // padded lanes: distinct dummy keys
-      w1[u] = e < b1 ? __dmul_rn(w1[u], part) : 0.0;
-      w2[u] = e < b1 ? __dmul_rn(part, part) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const unsigned peers = __match_any_sync(0xffffffffu, row[u]);
-      const int rk = __popc(peers & lt);
-      const int rounds = __reduce_max_sync(0xffffffffu, rk);
-      for (int j = 0; j <= rounds; ++j) {
-        if (rk == j && row[u] >= 0) {
-          double2 v = my[row[u]];
-          v.x += w1[u];
-          v.y += w2[u];
-          my[row[u]] = v;
-        }
-        __syncwarp();
-      }
-    }
-  }
-  __syncthreads();
-  for (int64_t k = threadIdx.x; k < dim; k += blockDim.x) {
-    double2 s = acc[k];
-    for (int w = 1; w < nw; ++w) {
-      const double2 v = acc[(int64_t)w * dim + k];
-      s.x += v.x;
-      s.y += v.y;
-    }
-    cta_part[(int64_t)blockIdx.x * dim + k] = s;
-  }
-}
-
-__global__ void ccd_priv_finish(const CcdParams p, const double2 *__restrict__ cta_part,
-                                int nblocks) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.dim;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double num = 0.0, den = 0.0;
-    for (int b = 0; b < nblocks; ++b) {
-      const double2 v = cta_part[(int64_t)b * p.dim + i];
-      num += v.x;
-      den += v.y;
-    }
-    if (p.numden) {
-      p.numden[i] = num;
-      p.numden[p.dim + i] = den;
-    } else {
-      const double dr = den + p.reg;
-      if (dr > 0.0) p.cols[p.mode][i] = num / dr;
-    }
-  }
-}
-
 }  // namespace cpfit
 
 using namespace cpfit;
@@ -547,70 +438,21 @@ static unsigned ccd_task_grid(int64_t ntasks) {
   return (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
 }
 
-// Pass selection (CPFIT_CCD_PATH=task|flat|priv overrides, for tuning):
-// the flat segmented pass for orders 2..5 (fold fused in identity order,
-// rhat through the permutation otherwise), the task-table pass beyond.
-enum { CCD_PATH_TASK = 0, CCD_PATH_FLAT = 1, CCD_PATH_PRIV = 2 };
-constexpr size_t CCD_PRIV_SMEM = 200 * 1024;
+// Pass selection (CPFIT_CCD_PATH=task forces the task-table pass, for tests):
+// the flat segmented pass for orders 2..5, the task-table pass beyond.
+enum { CCD_PATH_TASK = 0, CCD_PATH_FLAT = 1 };
 
-static int ccd_priv_warps(int64_t dim) {
-  int64_t nw = (int64_t)CCD_PRIV_SMEM / (dim * (int64_t)sizeof(double2));
-  return (int)(nw > 8 ? 8 : nw);
-}
-
-static int ccd_path(cpfit_pattern *pt, int mode, int fold) {
+static int ccd_path(cpfit_pattern *pt) {
   const char *env = getenv("CPFIT_CCD_PATH");
-  const int64_t dim = pt->dims[mode];
-  const bool priv_ok = !fold && pt->order >= 2 && pt->order <= 4 && ccd_priv_warps(dim) >= 4;
-  if (env) {
-    if (!strcmp(env, "task")) return CCD_PATH_TASK;
-    if (!strcmp(env, "priv") && priv_ok) return CCD_PATH_PRIV;
-    return pt->order >= 2 && pt->order <= 5 ? CCD_PATH_FLAT : CCD_PATH_TASK;
-  }
-  // measured at cfg 3 (mode 2, 2,182 rows): flat-through-permutation 1.87 ms,
-  // privatised 2.3 ms (five warps per SM hold the accumulators: latency-bound),
-  // so the privatised pass is opt-in
+  if (env && !strcmp(env, "task")) return CCD_PATH_TASK;
   return pt->order >= 2 && pt->order <= 5 ? CCD_PATH_FLAT : CCD_PATH_TASK;
-}
-
-static int64_t ccd_priv_per_cta(int64_t nnz) {
-  const int64_t nblocks = num_sms();
-  int64_t per_cta = (nnz + nblocks - 1) / nblocks;
-  return (per_cta + 32 * CCD_PRIV_U - 1) / (32 * CCD_PRIV_U) * (32 * CCD_PRIV_U);
-}
-
-template <int NO, int MODE>
-static int ccd_priv_launch1(const CcdParams &p, int64_t per_cta, double2 *part, int nw,
-                            size_t smem, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    CPFIT_CUDA(cudaFuncSetAttribute(ccd_priv_kernel<NO, MODE>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)CCD_PRIV_SMEM));
-    attr_set = true;
-  }
-  ccd_priv_kernel<NO, MODE><<<num_sms(), nw * 32, smem, s>>>(p, per_cta, part);
-  CPFIT_LAUNCH_CHECK("ccd_priv");
-  return CPFIT_OK;
-}
-
-static int ccd_priv_launch(int order, int mode, const CcdParams &p, int64_t per_cta,
-                           double2 *part, int nw, size_t smem, cudaStream_t s) {
-#define CCD_PRIV_CASE(NO, M) \
-  if (order == NO && mode == M) return ccd_priv_launch1<NO, M>(p, per_cta, part, nw, smem, s);
-  CCD_PRIV_CASE(2, 0) CCD_PRIV_CASE(2, 1)
-  CCD_PRIV_CASE(3, 0) CCD_PRIV_CASE(3, 1) CCD_PRIV_CASE(3, 2)
-  CCD_PRIV_CASE(4, 0) CCD_PRIV_CASE(4, 1) CCD_PRIV_CASE(4, 2) CCD_PRIV_CASE(4, 3)
-#undef CCD_PRIV_CASE
-  set_error("privatised CCD pass: order %d mode %d not instantiated", order, mode);
-  return CPFIT_EINVAL;
 }
 
 extern "C" {
 
 int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rhat,
-                   int fold, const double *const *fold_sub, double reg, double *numden,
-                   void *stream) {
+                   int rhat_sorted, const double *const *fold_sub,
+                   const double *const *fold_add, double reg, double *numden, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (!pt || mode < 0 || mode >= pt->order) {
     set_error("mode %d out of range", mode);
@@ -621,14 +463,16 @@ int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rha
     return CPFIT_EINVAL;
   }
   for (int q = 0; q < pt->order; ++q)
-    if (!cols[q] || (fold_sub && !fold_sub[q])) {
+    if (!cols[q] || (fold_sub && !fold_sub[q]) || (fold_add && !fold_add[q])) {
       set_error("column of mode %d is null", q);
       return CPFIT_EINVAL;
     }
   CPFIT_TRY(ensure_layout(pt, mode, s));
   CpfitModeLayout &L = pt->modes[mode];
-  if (fold && L.perm) {
-    set_error("fused fold needs the identity (canonical) order: mode 0 only");
+  const bool sorted = rhat_sorted || !L.perm;  // identity order: canonical == sorted
+  const bool fold = fold_sub || fold_add;
+  if (fold && !sorted) {
+    set_error("folding needs rhat in the mode-sorted order (rhat_sorted = 1)");
     return CPFIT_EINVAL;
   }
   CcdParams p{};
@@ -639,10 +483,11 @@ int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rha
   for (int q = 0; q < pt->order; ++q) {
     p.cols[q] = cols[q];
     p.sub[q] = fold_sub ? fold_sub[q] : nullptr;
+    p.add[q] = fold_add ? fold_add[q] : nullptr;
     p.sidx[q] = L.sorted_idx[q];
     p.coords[q] = pt->coords[q];
   }
-  p.perm = L.perm;
+  p.perm = sorted ? nullptr : L.perm;
   p.task_begin = L.task_begin;
   p.task_row = L.task_row;
   p.task_slot = L.task_slot;
@@ -651,6 +496,7 @@ int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rha
   p.reg = reg;
   p.fold = fold;
   p.has_sub = fold_sub != nullptr;
+  p.has_add = fold_add != nullptr;
   p.numden = numden;
   if (numden) CPFIT_CUDA(cudaMemsetAsync(numden, 0, 2 * (size_t)p.dim * sizeof(double), s));
   if (pt->nnz == 0) {
@@ -660,19 +506,7 @@ int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rha
     }
     return CPFIT_OK;
   }
-  const int path = ccd_path(pt, mode, fold);
-  if (path == CCD_PATH_PRIV) {
-    // few rows: canonical order, per-warp shared-memory accumulators
-    const int nw = ccd_priv_warps(p.dim);
-    const size_t smem = (size_t)nw * p.dim * sizeof(double2);
-    const int64_t per_cta = ccd_priv_per_cta(pt->nnz);
-    Scratch<double2> part(s);
-    CPFIT_TRY(part.alloc((size_t)num_sms() * p.dim));
-    CPFIT_TRY(ccd_priv_launch(pt->order, mode, p, per_cta, part.ptr, nw, smem, s));
-    ccd_priv_finish<<<grid_for(p.dim, 128), 128, 0, s>>>(p, part.ptr, num_sms());
-    CPFIT_LAUNCH_CHECK("ccd_priv_finish");
-    return CPFIT_OK;
-  }
+  const int path = ccd_path(pt);
   if (path == CCD_PATH_FLAT) {
     const int64_t nchunks = (pt->nnz + CCD_FLAT_CHUNK - 1) / CCD_FLAT_CHUNK;
     Scratch<double2> pf(s), pl(s);
@@ -693,6 +527,13 @@ int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rha
     CPFIT_LAUNCH_CHECK("ccd_flat_fixup");
     return CPFIT_OK;
   }
+  // task-table pass; a fold is a separate elementwise launch in sorted order
+  if (fold) {
+    CcdParams f = p;
+    for (int q = 0; q < pt->order; ++q) f.coords[q] = L.sorted_idx[q];
+    ccd_fold_kernel<<<grid_for(pt->nnz, 256, 4), 256, 0, s>>>(pt->order, pt->nnz, f);
+    CPFIT_LAUNCH_CHECK("ccd_fold");
+  }
   Scratch<double> slots(s);
   if (L.nslots > 0) CPFIT_TRY(slots.alloc(2 * L.nslots));
   p.slots = slots.ptr;
@@ -701,10 +542,7 @@ int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rha
     ccd_empty_rows<<<grid_for(p.dim, 256), 256, 0, s>>>(p.dim, L.offsets, reg, cols[mode]);
     CPFIT_LAUNCH_CHECK("ccd_empty_rows");
   }
-  if (fold)
-    ccd_rows_kernel<true><<<ccd_task_grid(L.ntasks), 256, 0, s>>>(p);
-  else
-    ccd_rows_kernel<false><<<ccd_task_grid(L.ntasks), 256, 0, s>>>(p);
+  ccd_rows_kernel<<<ccd_task_grid(L.ntasks), 256, 0, s>>>(p);
   CPFIT_LAUNCH_CHECK("ccd_rows");
   if (L.nsplit > 0) {
     ccd_combine<<<grid_for(L.nsplit * 32, 256), 256, 0, s>>>(p, L.split_row, L.split_slot,
@@ -714,29 +552,31 @@ int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rha
   return CPFIT_OK;
 }
 
-int cpfit_ccd_fold(cpfit_pattern *pt, const double *const *sub, const double *const *add,
-                   double *rhat, void *stream) {
+int cpfit_ccd_fold(cpfit_pattern *pt, int mode, const double *const *sub,
+                   const double *const *add, double *rhat, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (!pt) {
-    set_error("null pattern");
+  if (!pt || mode < -1 || mode >= pt->order) {
+    set_error("bad pattern or mode %d", mode);
     return CPFIT_EINVAL;
   }
   if (pt->nnz == 0 || (!sub && !add)) return CPFIT_OK;
   CcdParams p{};
   p.order = pt->order;
   p.nnz = pt->nnz;
+  if (mode >= 0) CPFIT_TRY(ensure_layout(pt, mode, s));
   for (int q = 0; q < pt->order; ++q) {
     if ((sub && !sub[q]) || (add && !add[q])) {
       set_error("column of mode %d is null", q);
       return CPFIT_EINVAL;
     }
     p.sub[q] = sub ? sub[q] : nullptr;
-    p.cols[q] = add ? const_cast<double *>(add[q]) : nullptr;
-    p.coords[q] = pt->coords[q];
+    p.add[q] = add ? add[q] : nullptr;
+    p.coords[q] = mode >= 0 ? pt->modes[mode].sorted_idx[q] : pt->coords[q];
   }
   p.has_sub = sub != nullptr;
+  p.has_add = add != nullptr;
   p.rhat = rhat;
-  ccd_fold_kernel<<<grid_for(pt->nnz, 256, 4), 256, 0, s>>>(pt->order, pt->nnz, p, add != nullptr);
+  ccd_fold_kernel<<<grid_for(pt->nnz, 256, 4), 256, 0, s>>>(pt->order, pt->nnz, p);
   CPFIT_LAUNCH_CHECK("ccd_fold");
   return CPFIT_OK;
 }

@@ -231,35 +231,38 @@ class DeviceBackend:
     def ccd_begin(self, shard, factors):
         torch = self.torch
         from .losses import tttp_affine
+        from .optim import _ccd_col_ptrs, _ccd_lean, _ccd_rhat_copies
         cols = [f.t().contiguous() for f in factors]  # R x I_n
-        rhat = tttp_affine(shard, factors, -1.0, 1.0, torch.float64)  # t - model
-        return {"cols": cols, "rhat": rhat, "prev": None, "shard": shard}
-
-    def _ccd_ptrs(self, state, r):
-        import ctypes
-
-        from . import _lib
-        arr = _lib.ptr_array([c[r].data_ptr() for c in state["cols"]])
-        return arr, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
+        resid = tttp_affine(shard, factors, -1.0, 1.0, torch.float64)  # t - model
+        lean = _ccd_lean(shard)
+        old = [torch.empty(d, dtype=torch.float64, device=resid.device) for d in shard.shape]
+        return {"cols": cols, "rh": _ccd_rhat_copies(shard, resid, lean), "lean": lean,
+                "old": old, "old_ptrs": _ccd_col_ptrs(old), "prev": None, "shard": shard}
 
     def ccd_numden(self, shard, state, r, mode):
-        """Local (num, den) of column r on `mode`; mode 0 first re-forms the
-        shard's rhat for column r (fused fold, csrc/ccd.cu)."""
+        """Local (num, den) of column r on `mode`; the pass first re-forms the
+        shard's rhat copy of this mode for column r (csrc/ccd.cu)."""
         import ctypes
 
         from . import _lib
-        from .optim import _stream
-        keep, ptrs = self._ccd_ptrs(state, r)
-        state["cur"] = (keep, ptrs)
-        nd = self.torch.empty(2 * shard.shape[mode], dtype=self.torch.float64,
-                              device=state["rhat"].device)
-        sub = state["prev"][1] if (mode == 0 and state["prev"] is not None) else None
-        _lib.check(_lib.load().cpfit_ccd_step(
-            shard.device_pattern().handle, mode, ptrs,
-            ctypes.c_void_p(state["rhat"].data_ptr()), 1 if mode == 0 else 0, sub, 0.0,
-            ctypes.c_void_p(nd.data_ptr()), _stream()), "ccd_step")
+        from .optim import _ccd_col_ptrs, _stream
+        keep, ptrs = _ccd_col_ptrs(state["cols"], r)
         if mode == 0:
-            state["prev"] = None
+            state["cur"] = (keep, ptrs)
+            for n, o in enumerate(state["old"]):
+                o.copy_(state["cols"][n][r])
+        nd = self.torch.empty(2 * shard.shape[mode], dtype=self.torch.float64,
+                              device=state["rh"][0].device)
+        sub = state["prev"][1] if state["prev"] is not None else None
+        if state["lean"]:
+            f = mode == 0
+            args = (state["rh"][0], 0, sub if f else None, ptrs if f else None)
+        else:
+            args = (state["rh"][mode], 1, sub, state["old_ptrs"][1])
+        _lib.check(_lib.load().cpfit_ccd_step(
+            shard.device_pattern().handle, mode, ptrs, ctypes.c_void_p(args[0].data_ptr()),
+            args[1], args[2], args[3], 0.0, ctypes.c_void_p(nd.data_ptr()), _stream()),
+            "ccd_step")
         return nd
 
     def ccd_apply(self, shard, state, r, mode, nd, reg):
@@ -279,10 +282,10 @@ class DeviceBackend:
 
         from . import _lib
         from .optim import _stream
-        if state["prev"] is not None and state["rhat"].numel():
+        if state["prev"] is not None and state["rh"][0].numel():
             _lib.check(_lib.load().cpfit_ccd_fold(
-                state["shard"].device_pattern().handle, state["prev"][1], None,
-                ctypes.c_void_p(state["rhat"].data_ptr()), _stream()), "ccd_fold")
+                state["shard"].device_pattern().handle, -1, state["prev"][1], None,
+                ctypes.c_void_p(state["rh"][0].data_ptr()), _stream()), "ccd_fold")
         for n, c in enumerate(state["cols"]):
             factors[n] = c.t().contiguous()
 

@@ -320,42 +320,90 @@ def _like(ref, a):
 # ---------------------------------------------------------------------------
 # coordinate minimization
 
-def _ccd_col_ptrs(cols, r):
-    """Pointer array to column r of every mode (cols[n] is R x I_n)."""
-    arr = _lib.ptr_array([c[r].data_ptr() for c in cols])
+def _ccd_col_ptrs(cols, r=None):
+    """Pointer array to column r of every mode (cols[n] is R x I_n), or to the
+    vectors themselves when r is None."""
+    arr = _lib.ptr_array([(c if r is None else c[r]).data_ptr() for c in cols])
     return arr, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
 
 
-def _ccd_ls_device(t: SparseTensor, F, reg: float):
+def _ccd_rhat_copies(t: SparseTensor, resid, lean: bool):
+    """rhat copies: mode n's in its mode-sorted order (mode 0: canonical), or
+    the canonical one only (lean: modes > 0 read it through the permutation)."""
+    torch = _torch()
+    if lean:
+        return [resid]
+    copies = [resid]
+    for n in range(1, t.order):
+        out = torch.empty_like(resid)
+        if t.nnz:
+            _lib.check(_lib.load().cpfit_permute_values(
+                t.device_pattern().handle, n, _dtype_code(torch.float64),
+                ctypes.c_void_p(resid.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                _stream()), "permute_values")
+        copies.append(out)
+    return copies
+
+
+def _ccd_lean(t: SparseTensor) -> bool:
+    """One canonical rhat when the per-mode copies would not fit comfortably."""
+    torch = _torch()
+    need = (t.order - 1) * t.nnz * 8
+    try:
+        free, _ = torch.cuda.mem_get_info()
+    except RuntimeError:
+        return False
+    return need > free // 2
+
+
+def _ccd_ls_device(t: SparseTensor, F, reg: float, lean: bool | None = None):
     """CCD++ least-squares sweep on device factors (list of f64 CUDA tensors).
 
     Column r keeps rhat = resid + (rank-one term of column r) on the device:
     it is every mode's rho of the reference (optim.py:254) in exact
-    arithmetic, so each (r, mode) update is one segmented (num, den) pass and
-    the residual is re-formed once per column, fused into the mode-0 pass
-    (csrc/ccd.cu).  Returns the residual t - model."""
+    arithmetic, so each (r, mode) update is one segmented (num, den) pass.
+    Every mode holds its own copy of rhat in its mode-sorted order and
+    re-forms it for column r inside its own pass (csrc/ccd.cu).  Returns the
+    residual t - model."""
     torch = _torch()
     order = t.order
     rank = F[0].shape[1]
     L = _lib.load()
     pat = t.device_pattern()
+    if lean is None:
+        lean = _ccd_lean(t)
     cols = [f.t().contiguous() for f in F]  # R x I_n: column r contiguous
-    rhat = tttp_affine(t, F, -1.0, 1.0, torch.float64)  # t - model
+    resid = tttp_affine(t, F, -1.0, 1.0, torch.float64)  # t - model
+    rh = _ccd_rhat_copies(t, resid, lean)
+    old = [torch.empty(d, dtype=torch.float64, device=resid.device) for d in t.shape]
+    old_keep, old_ptrs = _ccd_col_ptrs(old)
     prev = None
     for r in range(rank):
         keep, ptrs = _ccd_col_ptrs(cols, r)
-        for mode in range(order):
-            sub = prev[1] if (mode == 0 and prev is not None) else None
-            _lib.check(L.cpfit_ccd_step(pat.handle, mode, ptrs, ctypes.c_void_p(rhat.data_ptr()),
-                                        1 if mode == 0 else 0, sub, float(reg), None, _stream()),
-                       "ccd_step")
+        sub = prev[1] if prev is not None else None
+        if lean:
+            # canonical copy only: re-formed in the mode-0 pass (identity order,
+            # column r untouched there, so cols themselves are the "old" values)
+            for mode in range(order):
+                f = mode == 0
+                _lib.check(L.cpfit_ccd_step(
+                    pat.handle, mode, ptrs, ctypes.c_void_p(rh[0].data_ptr()), 0,
+                    sub if f else None, ptrs if f else None, float(reg), None, _stream()),
+                    "ccd_step")
+        else:
+            for n in range(order):
+                old[n].copy_(cols[n][r])
+            for mode in range(order):
+                _lib.check(L.cpfit_ccd_step(
+                    pat.handle, mode, ptrs, ctypes.c_void_p(rh[mode].data_ptr()), 1, sub,
+                    old_ptrs, float(reg), None, _stream()), "ccd_step")
         prev = (keep, ptrs)
     if prev is not None:
-        _lib.check(L.cpfit_ccd_fold(pat.handle, prev[1], None, ctypes.c_void_p(rhat.data_ptr()),
-                                    _stream()), "ccd_fold")
+        _lib.check(L.cpfit_ccd_fold(pat.handle, -1, prev[1], None,
+                                    ctypes.c_void_p(rh[0].data_ptr()), _stream()), "ccd_fold")
     for n in range(order):
         F[n] = cols[n].t().contiguous()
-    return rhat
+    return rh[0]
 
 
 def ccd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,

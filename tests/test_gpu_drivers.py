@@ -251,13 +251,17 @@ def test_cfg2_scaled_sweeps_vs_oracle():
         assert rel(st.factors[n], fs[n]) < 1e-10
 
 
-@pytest.mark.parametrize("path", ["task", "flat", "priv"])
+@pytest.mark.parametrize("path", ["task", "flat", "lean"])
 def test_ccd_kernel_paths_vs_oracle(path, monkeypatch):
     """Each CCD++ pass implementation (task table, flat segmented scan, and the
-    privatised canonical pass for small modes) against the oracle on a
-    Zipf-skewed cfg 3-shaped instance (long split rows, empty rows, a small
-    mode), bitwise run-to-run deterministic."""
-    monkeypatch.setenv("CPFIT_CCD_PATH", path)
+    memory-lean single canonical rhat read through the permutations) against
+    the oracle on a Zipf-skewed cfg 3-shaped instance (long split rows, empty
+    rows, a small mode), bitwise run-to-run deterministic."""
+    from paper_1910_02371_b200 import optim
+    if path == "lean":
+        monkeypatch.setattr(optim, "_ccd_lean", lambda t: True)
+    else:
+        monkeypatch.setenv("CPFIT_CCD_PATH", path)
     shape, keys, values = synth.cfg3(nnz=400_000, shape=(48_019, 1_777, 218))
     rng = np.random.default_rng(4)
     factors = [rng.random((d, 6)) / np.sqrt(6) for d in shape]
