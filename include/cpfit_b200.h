@@ -213,7 +213,7 @@ int cpfit_gather_values(int dtype, int64_t n, const int32_t *idx,
 /* ---- reductions and updates ------------------------------------------- */
 
 /* Deterministic (fixed-order) reductions in fp64, result copied to the host:
- * op 0: sum x^2;  op 1: sum (x - y)^2;  op 2: sum x*y.
+ * op 0: sum x^2;  op 1: sum (x - y)^2;  op 2: sum x*y;  op 3: sum x.
  * Serves objective / rmse (losses.py:126-150, optim.py:642-652). */
 int cpfit_reduce(int op, int dtype, int64_t n, const void *x, const void *y,
                  double *result, void *stream);
@@ -265,6 +265,40 @@ int cpfit_ccd_fold(cpfit_pattern *p, int mode, const double *const *sub,
                    const double *const *add, double *rhat, void *stream);
 int cpfit_ccd_finalize(int64_t dim, const double *numden, double reg,
                        double *col, void *stream);
+
+/* ---- generalized losses (losses.py:22-104) ---------------------------- */
+/* Loss ids: 0 = least squares (phi = (t - m)^2, dphi = 2 (m - t), d2phi = 2),
+ * 1 = Poisson log link (phi = exp(m~) - t m, dphi = exp(m~) - t, d2phi =
+ * exp(m~), m~ = min(m, 50): POISSON_EXP_CLAMP, losses.py:19-91).  *clamped
+ * (host, nullable) receives the number of entries with m > 50 (the
+ * reference's diagnostics["exp_clamped"] counts one per entry per exp call).
+ *
+ * cpfit_tttp_loss: the derivative tensors at the model of `factors` on the
+ * pattern (model_at_observed + derivative_tensors, losses.py:107-123) in one
+ * pass: TTTP with the loss epilogue, dphi / d2phi written in canonical order.
+ * cpfit_loss_eval: elementwise phi / dphi / d2phi (outputs nullable). */
+int cpfit_tttp_loss(cpfit_pattern *p, int dtype, int rank, const void *t_vals,
+                    const void *const *factors, int loss, void *dphi, void *d2phi,
+                    int64_t *clamped, void *stream);
+int cpfit_loss_eval(int loss, int dtype, int64_t n, const void *t, const void *m,
+                    void *phi, void *dphi, void *d2phi, int64_t *clamped,
+                    void *stream);
+
+/* Inner-Newton CCD++ column step for generalized losses (optim.py:269-294),
+ * fp64, canonical entry order.  cpfit_ccd_gen_weights: part_e = prod_{p !=
+ * mode} cols[p][i_p(e)], w1 = part * dphi(t, model), w2 = part^2 * d2phi;
+ * the row sums num / den come from cpfit_mttkrp (R = 1, unit columns);
+ * cpfit_ccd_gen_update: delta = -(num + 2 reg col) / (den + 2 reg) where the
+ * denominator is > 0, else 0, col += delta; cpfit_ccd_gen_model:
+ * model_e += part_e * delta[i_mode(e)]. */
+int cpfit_ccd_gen_weights(cpfit_pattern *p, int mode, int loss,
+                          const double *const *cols, const double *t,
+                          const double *model, double *w1, double *w2,
+                          double *part, int64_t *clamped, void *stream);
+int cpfit_ccd_gen_update(int64_t dim, const double *num, const double *den,
+                         double reg, double *col, double *delta, void *stream);
+int cpfit_ccd_gen_model(cpfit_pattern *p, int mode, const double *part,
+                        const double *delta, double *model, void *stream);
 
 /* Batched regularised SPD solves without a tensor pattern:
  * (G_i + reg I) x_i = rhs_i for i < nrows, G_i = gram + i * gram_stride

@@ -163,6 +163,35 @@ inline int pick_vec(int rank, const void *const *ptrs, int n) {
   return vec;
 }
 
+// per-mode column pointers + coordinate arrays passed by value to kernels
+struct CpfitCols {
+  const double *col[CPFIT_MAXN];
+  const int32_t *idx[CPFIT_MAXN];
+};
+
+// ---- elementwise losses (losses.py:41-91) -----------------------------------
+// loss 0: least squares  phi = (t - m)^2, dphi = 2 (m - t), d2phi = 2
+// loss 1: Poisson log link  phi = exp(m~) - t m, dphi = exp(m~) - t,
+//         d2phi = exp(m~), with m~ = min(m, 50) (POISSON_EXP_CLAMP);
+// returns whether m was clamped (the reference counts those events).
+#define CPFIT_POISSON_CLAMP 50.0
+__device__ __forceinline__ bool loss_eval1(int loss, double t, double m, double &phi,
+                                           double &d1, double &d2) {
+  if (loss == 1) {
+    const bool cl = m > CPFIT_POISSON_CLAMP;
+    const double e = exp(cl ? CPFIT_POISSON_CLAMP : m);
+    phi = __dsub_rn(e, __dmul_rn(t, m));
+    d1 = __dsub_rn(e, t);
+    d2 = e;
+    return cl;
+  }
+  const double d = __dsub_rn(t, m);
+  phi = __dmul_rn(d, d);
+  d1 = __dmul_rn(2.0, __dsub_rn(m, t));
+  d2 = 2.0;
+  return false;
+}
+
 // ---- device scan (exclusive, int64 out) -----------------------------------
 // out[i] = sum_{j<i} in[j] for i in [0, n]; out has n+1 entries (out[n] = total).
 template <typename Tin>

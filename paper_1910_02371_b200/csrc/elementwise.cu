@@ -160,7 +160,7 @@ __global__ void gather_values_kernel(const int32_t *__restrict__ idx, int64_t n,
 constexpr int RED_THREADS = 256;
 constexpr int RED_BLOCKS = 592;  // 4 x 148 SMs; fixed so the order never varies
 
-template <typename T, int OP>  // OP 0: sum x^2, 1: sum (x - y)^2, 2: sum x*y
+template <typename T, int OP>  // OP 0: sum x^2, 1: sum (x - y)^2, 2: sum x*y, 3: sum x
 __global__ void __launch_bounds__(RED_THREADS)
 reduce_partials(int64_t n, const T *__restrict__ x, const T *__restrict__ y,
                 double *__restrict__ partial) {
@@ -171,6 +171,7 @@ reduce_partials(int64_t n, const T *__restrict__ x, const T *__restrict__ y,
     if (OP == 0) acc += a * a;
     if (OP == 1) { const double d = a - (double)y[k]; acc += d * d; }
     if (OP == 2) acc += a * (double)y[k];
+    if (OP == 3) acc += a;
   }
   __shared__ double sm[RED_THREADS];
   sm[threadIdx.x] = acc;
@@ -203,6 +204,7 @@ static int run_reduce(int op, int64_t n, const T *x, const T *y, double *result,
   if (op == 0) reduce_partials<T, 0><<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, x, y, part.ptr);
   if (op == 1) reduce_partials<T, 1><<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, x, y, part.ptr);
   if (op == 2) reduce_partials<T, 2><<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, x, y, part.ptr);
+  if (op == 3) reduce_partials<T, 3><<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, x, y, part.ptr);
   CPFIT_LAUNCH_CHECK("reduce_partials");
   reduce_final<<<1, 1024, 0, s>>>(part.ptr, RED_BLOCKS, part.ptr + RED_BLOCKS);
   CPFIT_LAUNCH_CHECK("reduce_final");
@@ -347,7 +349,7 @@ int cpfit_gather_values(int dtype, int64_t n, const int32_t *idx, const void *in
 int cpfit_reduce(int op, int dtype, int64_t n, const void *x, const void *y, double *result,
                  void *stream) {
   *result = 0.0;
-  if (op < 0 || op > 2) { set_error("unknown reduction %d", op); return CPFIT_EINVAL; }
+  if (op < 0 || op > 3) { set_error("unknown reduction %d", op); return CPFIT_EINVAL; }
   if (n <= 0) return CPFIT_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == CPFIT_F64)

@@ -14,10 +14,14 @@ extern template int dispatch_mttkrp<float>(const MttkrpParams<float> &, int, cud
 template <typename T>
 static int run_tttp(cpfit_pattern *pt, int rank, const void *vals, const void *const *factors,
                     void *out, cudaStream_t s, int epi = 0, double alpha = 0.0,
-                    double beta = 0.0, int64_t begin = 0, int64_t end = -1) {
+                    double beta = 0.0, int64_t begin = 0, int64_t end = -1, int loss = 0,
+                    void *out2 = nullptr, unsigned long long *clamped = nullptr) {
   if (end < 0) end = pt->nnz;
   TttpParams<T> p{};
   p.epi = epi;
+  p.loss = loss;
+  p.out2 = out2 ? (T *)out2 + begin : nullptr;
+  p.clamped = clamped;
   p.alpha = (T)alpha;
   p.beta = (T)beta;
   p.rank = rank;
@@ -169,6 +173,40 @@ int cpfit_tttp_axpby(cpfit_pattern *p, int dtype, int rank, const void *vals,
   if (dtype == CPFIT_F32) return run_tttp<float>(p, rank, vals, factors, out, s, 1, alpha, beta);
   set_error("unknown dtype %d", dtype);
   return CPFIT_EINVAL;
+}
+
+int cpfit_tttp_loss(cpfit_pattern *p, int dtype, int rank, const void *t_vals,
+                    const void *const *factors, int loss, void *dphi, void *d2phi,
+                    int64_t *clamped, void *stream) {
+  if (!p) { set_error("null pattern"); return CPFIT_EINVAL; }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  if (loss < 0 || loss > 1) { set_error("unknown loss id %d", loss); return CPFIT_EINVAL; }
+  if (p->nnz > 0 && (!t_vals || !dphi || !d2phi)) { set_error("null array"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch<unsigned long long> cnt(s);
+  if (clamped) {
+    CPFIT_TRY(cnt.alloc(1));
+    CPFIT_CUDA(cudaMemsetAsync(cnt.ptr, 0, sizeof(unsigned long long), s));
+  }
+  int st;
+  if (dtype == CPFIT_F64)
+    st = run_tttp<double>(p, rank, t_vals, factors, dphi, s, 2, 0.0, 0.0, 0, -1, loss, d2phi,
+                          cnt.ptr);
+  else if (dtype == CPFIT_F32)
+    st = run_tttp<float>(p, rank, t_vals, factors, dphi, s, 2, 0.0, 0.0, 0, -1, loss, d2phi,
+                         cnt.ptr);
+  else {
+    set_error("unknown dtype %d", dtype);
+    return CPFIT_EINVAL;
+  }
+  if (st != CPFIT_OK) return st;
+  if (clamped) {
+    unsigned long long h = 0;
+    CPFIT_CUDA(cudaMemcpyAsync(&h, cnt.ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CPFIT_CUDA(cudaStreamSynchronize(s));
+    *clamped = (int64_t)h;
+  }
+  return CPFIT_OK;
 }
 
 int cpfit_mttkrp(cpfit_pattern *p, int mode, int dtype, int rank, const void *vals,

@@ -47,8 +47,12 @@ struct TttpParams {
   const T *fac[CPFIT_MAXN];
   const T *vals;
   T *out;
-  int epi;        // 0: out = vals * acc;  1: out = alpha * acc + beta * vals
+  int epi;        // 0: out = vals * acc;  1: out = alpha * acc + beta * vals;
+                  // 2: loss derivatives at m = acc, t = vals: out = dphi, out2 = d2phi
   T alpha, beta;
+  int loss;                       // epi 2: loss id (common.cuh loss_eval1)
+  T *out2;                        // epi 2: d2phi
+  unsigned long long *clamped;    // epi 2: count of clamped model values (nullable)
 };
 
 // Gather the factor rows of U consecutive nonzero slots (j = (s0+u)*G + g)
@@ -210,8 +214,20 @@ __global__ void __launch_bounds__(256, CPFIT_TTTP_MINB) tttp_kernel(const TttpPa
         part[i] = keep + shfl_xor(send, half);
       }
     }
-    if (out_ok)
-      p.out[eo] = p.epi == 0 ? my_val * part[0] : p.alpha * part[0] + p.beta * my_val;
+    if (p.epi < 2) {
+      if (out_ok)
+        p.out[eo] = p.epi == 0 ? my_val * part[0] : p.alpha * part[0] + p.beta * my_val;
+    } else {
+      // fused loss epilogue (generalized losses, losses.py:117-123)
+      double phi, d1, d2;
+      const bool cl = out_ok && loss_eval1(p.loss, (double)my_val, (double)part[0], phi, d1, d2);
+      if (out_ok) {
+        p.out[eo] = (T)d1;
+        p.out2[eo] = (T)d2;
+      }
+      const unsigned nc = __ballot_sync(0xffffffffu, cl);
+      if (nc && lane == 0 && p.clamped) atomicAdd(p.clamped, (unsigned long long)__popc(nc));
+    }
 #pragma unroll
     for (int n = 0; n < NPM; ++n) my_idx[n] = nx_idx[n];
   }

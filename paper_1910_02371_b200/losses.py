@@ -1,13 +1,16 @@
 """Elementwise losses, derivative tensors and fit metrics (drop-in for the
 reference's losses.py).
 
-The least-squares loss -- the one the hot path serves -- is evaluated on the
-device: model values come from the TTTP kernel on the observation mask
-(losses.py:107-114), the derivative tensor 2(m - t) from the same kernel's
-affine epilogue, and sums from the library's fixed-order reductions.  Other
-registered losses (e.g. Poisson log-link, losses.py:51-91) are pluggable
-Python callables exactly as in the reference; their elementwise phi / dphi /
-d2phi run on host arrays while every tensor contraction stays on the GPU.
+The built-in losses (least squares and the Poisson log link, losses.py:41-91)
+are evaluated on the device: model values come from the TTTP kernel on the
+observation mask (losses.py:107-114), the derivative tensors from the same
+kernel's loss epilogue (cpfit_tttp_loss) or the elementwise cpfit_loss_eval,
+and sums from the library's fixed-order reductions; Poisson clamp events are
+counted on the device and added to ``diagnostics['exp_clamped']`` exactly as
+the reference's host exp() calls count them.  Losses registered by users stay
+pluggable Python callables exactly as in the reference (``device_id`` None):
+their elementwise phi / dphi / d2phi run on host arrays while every tensor
+contraction stays on the GPU.
 """
 
 from __future__ import annotations
@@ -37,6 +40,9 @@ class LossFunction:
     d2phi: Callable
     validate_data: Callable = lambda values: None
     diagnostics: dict = field(default_factory=dict)
+    # device evaluator of a built-in loss (csrc common.cuh loss_eval1): 0 = least
+    # squares, 1 = Poisson log link; None = host callables only
+    device_id: int | None = None
 
 
 def least_squares() -> LossFunction:
@@ -46,6 +52,7 @@ def least_squares() -> LossFunction:
         phi=lambda t, m: (t - m) ** 2,
         dphi=lambda t, m: 2.0 * (m - t),
         d2phi=lambda t, m: np.full_like(np.asarray(m, dtype=np.float64), 2.0),
+        device_id=0,
     )
 
 
@@ -67,7 +74,7 @@ def poisson_log_link() -> LossFunction:
 
     return LossFunction(ident="poisson", phi=lambda t, m: _exp(m) - t * m,
                         dphi=lambda t, m: _exp(m) - t, d2phi=lambda t, m: _exp(m),
-                        validate_data=validate_data, diagnostics=diagnostics)
+                        validate_data=validate_data, diagnostics=diagnostics, device_id=1)
 
 
 _REGISTRY: dict[str, Callable[[], LossFunction]] = {
@@ -125,6 +132,64 @@ def tttp_affine(t: SparseTensor, factors, alpha: float, beta: float, dtype=None)
     return out
 
 
+def _count_clamps(loss: LossFunction, n_clamped: int, calls: int) -> None:
+    """The reference's Poisson _exp adds the clamped count once per call
+    (losses.py:61-68); `calls` = how many of its exp() calls one device pass
+    stands for."""
+    if n_clamped and "exp_clamped" in loss.diagnostics:
+        loss.diagnostics["exp_clamped"] += calls * int(n_clamped)
+
+
+def device_derivatives(loss: LossFunction, t: SparseTensor, F, dtype=None):
+    """(dphi, d2phi, n_clamped): device tensors at the model of factors F on
+    t's pattern -- model_at_observed + derivative_tensors (losses.py:107-123)
+    in one TTTP pass with the loss epilogue.  Built-in losses only; the caller
+    books the clamp count (_count_clamps)."""
+    import torch
+    dtype = dtype or torch.float64
+    d1 = torch.empty(t.nnz, dtype=dtype, device=cuda_device())
+    d2 = torch.empty(t.nnz, dtype=dtype, device=cuda_device())
+    if t.nnz == 0:
+        return d1, d2, 0
+    dev = [_to_device(f, dtype) for f in F]
+    rank = next(f.shape[1] for f in dev if f is not None)
+    vals = t.device_values(dtype)
+    clamped = ctypes.c_int64(0)
+    _lib.check(_lib.load().cpfit_tttp_loss(
+        t.device_pattern().handle, _dtype_code(dtype), rank, ctypes.c_void_p(vals.data_ptr()),
+        _ptrs(dev), int(loss.device_id), ctypes.c_void_p(d1.data_ptr()),
+        ctypes.c_void_p(d2.data_ptr()), ctypes.byref(clamped) if loss.device_id == 1 else None,
+        ctypes.c_void_p(current_stream())), "tttp_loss")
+    return d1, d2, clamped.value
+
+
+def _loss_eval(loss: LossFunction, tv, mv, phi=False, d1=False, d2=False):
+    """Elementwise phi / dphi / d2phi of device arrays (cpfit_loss_eval)."""
+    import torch
+    outs = [torch.empty_like(mv) if want else None for want in (phi, d1, d2)]
+    clamped = ctypes.c_int64(0)
+    _lib.check(_lib.load().cpfit_loss_eval(
+        int(loss.device_id), _dtype_code(mv.dtype), mv.numel(), ctypes.c_void_p(tv.data_ptr()),
+        ctypes.c_void_p(mv.data_ptr()),
+        *[ctypes.c_void_p(0 if o is None else o.data_ptr()) for o in outs],
+        ctypes.byref(clamped) if loss.device_id == 1 else None,
+        ctypes.c_void_p(current_stream())), "loss_eval")
+    return outs, clamped.value
+
+
+def phi_sum(loss: LossFunction, t: SparseTensor, model: SparseTensor) -> float:
+    """sum phi(t, m) over the observed entries (losses.py:135)."""
+    if loss.device_id is None:
+        return float(np.sum(loss.phi(t.values, model.values)))
+    if t.nnz == 0:
+        return 0.0
+    import torch
+    (phi, _, _), n = _loss_eval(loss, t.device_values(torch.float64),
+                                model.device_values(torch.float64), phi=True)
+    _count_clamps(loss, n, 1)
+    return _reduce(3, phi)
+
+
 def ls_data_term(t: SparseTensor, factors, dtype=None) -> float:
     """sum (t - m)^2 over the observed entries (device)."""
     if t.nnz == 0:
@@ -154,11 +219,12 @@ def derivative_tensors(loss: LossFunction, t: SparseTensor, m: SparseTensor):
     """First and second derivative tensors on the shared pattern (losses.py:117-123)."""
     if t.nnz != m.nnz or not (t._shared is m._shared or np.array_equal(t.keys, m.keys)):
         raise ValueError("observed and model tensors must share a key set")
-    if loss.ident == "ls":
+    if loss.device_id is not None:
         import torch
-        tv = t.device_values(torch.float64)
-        mv = m.device_values(torch.float64)
-        return t.with_values(2.0 * (mv - tv)), t.with_values(torch.full_like(mv, 2.0))
+        (_, d1, d2), n = _loss_eval(loss, t.device_values(torch.float64),
+                                    m.device_values(torch.float64), d1=True, d2=True)
+        _count_clamps(loss, n, 2)  # dphi and d2phi each call exp()
+        return t.with_values(d1), t.with_values(d2)
     return (t.with_values(loss.dphi(t.values, m.values)),
             t.with_values(loss.d2phi(t.values, m.values)))
 
@@ -173,7 +239,7 @@ def objective(loss: LossFunction, t: SparseTensor, factors, reg: float = 0.0,
     else:
         if model is None:
             model = model_at_observed(t.observation_mask(), factors, threads=threads)
-        total = float(np.sum(loss.phi(t.values, model.values)))
+        total = phi_sum(loss, t, model)
     if reg:
         total += reg * factor_sq_norms(factors)
     return total

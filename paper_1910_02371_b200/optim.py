@@ -34,7 +34,7 @@ from .core import RngState, SparseTensor, _dtype_code, cuda_device, current_stre
 from .exceptions import NumericalError
 from .kernels import _ptrs, gram_blocks, mttkrp, solve_factor, tttp
 from .losses import (LossFunction, derivative_tensors, factor_sq_norms, get_loss,
-                     ls_data_term, model_at_observed, tttp_affine)
+                     ls_data_term, model_at_observed, phi_sum, tttp_affine)
 from .second_order import (BlockDiagPreconditioner, gn_step, gradient_blocks,  # noqa: F401
                            hessian_matvec, pcg_solve, rebalance_factors)
 from .trace import RunTrace
@@ -285,6 +285,11 @@ def als_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
             state.ls_rhs[mode] = rhss[mode].cpu().numpy() if host else rhss[mode]
         _write_back(state.factors, F)
         return
+    if loss.device_id is not None:
+        F = _to_dev_factors(state.factors)
+        _als_generalized_device(t, F, loss, cfg)
+        _write_back(state.factors, F)
+        return
     mask = t.observation_mask()
     for mode in range(t.order):
         phi2 = None
@@ -303,6 +308,45 @@ def als_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
             new = _as_np(state.factors[mode]) + delta
             state.factors[mode] = _like(state.factors[mode], new)
             rel = np.linalg.norm(delta) / max(np.linalg.norm(new), _TINY)
+            if rel < cfg.inner_tol:
+                break
+
+
+def _axpby(a: float, x, b: float, y, out):
+    _lib.check(_lib.load().cpfit_axpby(_dtype_code(x.dtype), x.numel(), float(a),
+                                       ctypes.c_void_p(x.data_ptr()), float(b),
+                                       ctypes.c_void_p(y.data_ptr()),
+                                       ctypes.c_void_p(out.data_ptr()), _stream()), "axpby")
+    return out
+
+
+def _als_generalized_device(t: SparseTensor, F, loss: LossFunction, cfg: SolverConfig):
+    """Inner-Newton alternating sweep of a built-in loss on device factors
+    (optim.py:208-229): per mode and inner step, the derivative tensors at the
+    current model in one fused TTTP pass (cpfit_tttp_loss), the gradient
+    MTTKRP(dphi) + 2 reg A, the phi2-weighted Gram + batched solve with 2 reg
+    on the diagonal, and the update; the inner stopping test reads two
+    fixed-order device norms."""
+    from .losses import _count_clamps, device_derivatives, sum_sq
+    torch = _torch()
+    for mode in range(t.order):
+        phi2 = None
+        for inner in range(cfg.inner_max):
+            d1, d2, n = device_derivatives(loss, t, F)
+            _count_clamps(loss, n, 2)
+            if phi2 is None or not cfg.freeze_curvature:
+                phi2 = t.with_values(d2)
+            grad = mttkrp(t.with_values(d1), F, mode)
+            _axpby(1.0, grad, 2.0 * cfg.reg, F[mode], grad)  # grad += 2 reg A (numpy order)
+            _axpby(-1.0, grad, 0.0, grad, grad)
+            try:
+                delta = solve_factor(phi2, F, grad, mode, reg=2.0 * cfg.reg,
+                                     row_batches=cfg.row_batches)
+            except NumericalError as err:
+                raise NumericalError(f"inner Newton solve failed: {err}") from err
+            new = torch.empty_like(F[mode])
+            F[mode] = _axpby(1.0, F[mode], 1.0, delta, new)
+            rel = math.sqrt(sum_sq(delta)) / max(math.sqrt(sum_sq(new)), _TINY)
             if rel < cfg.inner_tol:
                 break
 
@@ -414,8 +458,12 @@ def ccd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
         _ccd_ls_device(t, F, cfg.reg)
         _write_back(state.factors, F)
         return
-    # generalized loss: inner Newton per column (host elementwise, device-free
-    # bincounts as in the reference; out of the hot path)
+    if loss.device_id is not None:
+        F = _to_dev_factors(state.factors, _torch().float64)
+        _ccd_generalized_device(t, F, loss, cfg)
+        _write_back(state.factors, F)
+        return
+    # user-registered loss: inner Newton per column with its host callables
     coords = t.coords()
     factors = [_as_np(f).copy() for f in state.factors]
     order, rank = t.order, factors[0].shape[1]
@@ -446,14 +494,83 @@ def ccd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
         state.factors[n] = _like(state.factors[n], factors[n])
 
 
+def _ccd_generalized_device(t: SparseTensor, F, loss: LossFunction, cfg: SolverConfig):
+    """Inner-Newton CCD++ sweep of a built-in loss on device factors
+    (optim.py:269-294): per (r, mode, inner step) the weights part * dphi and
+    part^2 * d2phi at the current model (cpfit_ccd_gen_weights), their row
+    sums (two R = 1 MTTKRPs against unit columns), the damped-free Newton
+    column update and the model update; the stopping test reads two
+    fixed-order device norms."""
+    from .losses import _count_clamps, sum_sq, tttp_affine
+    torch = _torch()
+    L = _lib.load()
+    order = t.order
+    rank = F[0].shape[1]
+    dev = F[0].device
+    f64 = torch.float64
+    pat = t.device_pattern()
+    cols = [f.t().contiguous() for f in F]  # R x I_n
+    if t.nnz:
+        model = tttp_affine(t.observation_mask(), F, 1.0, 0.0, f64)
+    else:
+        model = torch.zeros(0, dtype=f64, device=dev)
+    tv = t.device_values(f64)
+    w1 = torch.empty_like(model)
+    w2 = torch.empty_like(model)
+    part = torch.empty_like(model)
+    ones = [torch.ones((d, 1), dtype=f64, device=dev) for d in t.shape]
+    ones_ptrs = _ptrs(ones)
+    deltas = [torch.empty(d, dtype=f64, device=dev) for d in t.shape]
+    clamped = ctypes.c_int64(0)
+    count = loss.device_id == 1
+    for r in range(rank):
+        keep, ptrs = _ccd_col_ptrs(cols, r)
+        for mode in range(order):
+            col = cols[mode][r]
+            num = torch.zeros((t.shape[mode], 1), dtype=f64, device=dev)
+            den = torch.zeros((t.shape[mode], 1), dtype=f64, device=dev)
+            for inner in range(cfg.inner_max):
+                if t.nnz:
+                    _lib.check(L.cpfit_ccd_gen_weights(
+                        pat.handle, mode, int(loss.device_id), ptrs,
+                        ctypes.c_void_p(tv.data_ptr()), ctypes.c_void_p(model.data_ptr()),
+                        ctypes.c_void_p(w1.data_ptr()), ctypes.c_void_p(w2.data_ptr()),
+                        ctypes.c_void_p(part.data_ptr()),
+                        ctypes.byref(clamped) if count else None, _stream()), "ccd_gen_weights")
+                    if count:
+                        _count_clamps(loss, clamped.value, 2)  # dphi and d2phi
+                    for w, out in ((w1, num), (w2, den)):
+                        _lib.check(L.cpfit_mttkrp(pat.handle, mode, _dtype_code(f64), 1,
+                                                  ctypes.c_void_p(w.data_ptr()), 0, ones_ptrs,
+                                                  ctypes.c_void_p(out.data_ptr()), _stream()),
+                                   "mttkrp")
+                delta = deltas[mode]
+                _lib.check(L.cpfit_ccd_gen_update(
+                    t.shape[mode], ctypes.c_void_p(num.data_ptr()),
+                    ctypes.c_void_p(den.data_ptr()), float(cfg.reg),
+                    ctypes.c_void_p(col.data_ptr()), ctypes.c_void_p(delta.data_ptr()),
+                    _stream()), "ccd_gen_update")
+                if t.nnz:
+                    _lib.check(L.cpfit_ccd_gen_model(
+                        pat.handle, mode, ctypes.c_void_p(part.data_ptr()),
+                        ctypes.c_void_p(delta.data_ptr()), ctypes.c_void_p(model.data_ptr()),
+                        _stream()), "ccd_gen_model")
+                rel = math.sqrt(sum_sq(delta)) / max(math.sqrt(sum_sq(col)), _TINY)
+                if rel < cfg.inner_tol:
+                    break
+    for n in range(order):
+        F[n] = cols[n].t().contiguous()
+
+
 # ---------------------------------------------------------------------------
 # stochastic gradient descent
 
 def _sgd_grads_device(t: SparseTensor, F, rate: float, rng: RngState, dtype,
-                      counter_offset: int = 0):
+                      counter_offset: int = 0, loss: LossFunction | None = None):
     """Sample (global Philox counter starts at counter_offset) and the per-mode
-    least-squares gradients MTTKRP(2(m - t)) on the device; returns
-    (grads, sample nnz)."""
+    gradients MTTKRP(dphi) on the device -- least squares 2(m - t) through the
+    TTTP affine epilogue, other built-in losses through its loss epilogue;
+    returns (grads, sample nnz)."""
     torch = _torch()
     from .sampling import sample_tensor
     code = _dtype_code(dtype)
@@ -463,7 +580,12 @@ def _sgd_grads_device(t: SparseTensor, F, rate: float, rng: RngState, dtype,
     if sampled.nnz == 0:
         return [torch.zeros((t.shape[m], rank), dtype=dtype, device=F[0].device)
                 for m in range(t.order)], 0
-    phi1 = tttp_affine(sampled, F, 2.0, -2.0, dtype)  # 2(m - t), losses.py:46
+    if loss is None or loss.device_id == 0:
+        phi1 = tttp_affine(sampled, F, 2.0, -2.0, dtype)  # 2(m - t), losses.py:46
+    else:
+        from .losses import _count_clamps, device_derivatives
+        phi1, _, n = device_derivatives(loss, sampled, F, dtype)
+        _count_clamps(loss, n, 1)  # sgd_sweep evaluates dphi only (optim.py:320)
     pat = sampled.device_pattern()
     grads = []
     for mode in range(t.order):
@@ -495,10 +617,12 @@ def _sgd_apply_device(F, grads, step: float, shrink: float, check: bool = True):
         F[mode] = new[mode]
 
 
-def _sgd_ls_device(t: SparseTensor, F, cfg: SolverConfig, rng: RngState):
-    """One SGD step on device factors F (list of CUDA tensors, replaced)."""
+def _sgd_ls_device(t: SparseTensor, F, cfg: SolverConfig, rng: RngState,
+                   loss: LossFunction | None = None):
+    """One SGD step on device factors F (list of CUDA tensors, replaced);
+    least squares unless a built-in `loss` is given."""
     shrink = 2.0 * cfg.step * cfg.reg * cfg.sample_rate
-    grads, n = _sgd_grads_device(t, F, cfg.sample_rate, rng, F[0].dtype)
+    grads, n = _sgd_grads_device(t, F, cfg.sample_rate, rng, F[0].dtype, loss=loss)
     _sgd_apply_device(F, grads, cfg.step, shrink, check=n > 0)
     return n
 
@@ -506,12 +630,12 @@ def _sgd_ls_device(t: SparseTensor, F, cfg: SolverConfig, rng: RngState):
 def sgd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
               cfg: SolverConfig, rng: RngState) -> None:
     """One sampled gradient step on all factors at once (optim.py:300-330)."""
-    if loss.ident == "ls":
+    if loss.device_id is not None:
         dtype = None
         if all(_is_torch(f) and f.dtype == _torch().float32 for f in state.factors):
             dtype = _torch().float32
         F = _to_dev_factors(state.factors, dtype)
-        _sgd_ls_device(t, F, cfg, rng)
+        _sgd_ls_device(t, F, cfg, rng, loss)
         _write_back(state.factors, F)
         return
     sampled = t.sample(cfg.sample_rate, rng)
@@ -554,7 +678,8 @@ def run(t: SparseTensor, cfg: SolverConfig, return_state: bool = False):
                   "shape": "x".join(str(d) for d in t.shape), "nnz": str(t.nnz)},
     )
     ls = loss.ident == "ls"
-    if ls:
+    on_device = loss.device_id is not None
+    if on_device:
         state.factors = _to_dev_factors(state.factors)
     mask = t.observation_mask()
     start = time.perf_counter()
@@ -569,7 +694,7 @@ def run(t: SparseTensor, cfg: SolverConfig, return_state: bool = False):
             metric = float(np.sqrt(data_term / max(t.nnz, 1)))
             return obj, metric
         model = model_at_observed(mask, state.factors, threads=cfg.threads)
-        data_term = float(np.sum(loss.phi(t.values, model.values)))
+        data_term = phi_sum(loss, t, model)
         obj = data_term + cfg.reg * factor_sq_norms(state.factors)
         return obj, data_term / max(t.nnz, 1)
 
@@ -609,7 +734,7 @@ def run(t: SparseTensor, cfg: SolverConfig, return_state: bool = False):
             if abs(prev_obj - obj) / max(abs(prev_obj), _TINY) < cfg.tol:
                 break
             prev_obj = obj
-    if ls:
+    if on_device:
         state.factors = [f.double().cpu().numpy() for f in state.factors]
     if return_state:
         return trace, state

@@ -100,6 +100,12 @@ class _DeviceDerivatives:
             self.phi1 = tttp_affine(t, F, 2.0, -2.0, torch.float64)
             self.phi2 = torch.full((t.nnz,), 2.0, dtype=torch.float64, device=cuda_device())
             return
+        if loss.device_id is not None:
+            # built-in loss: fused TTTP loss epilogue; its d2phi (exp) is >= 0
+            from .losses import _count_clamps, device_derivatives
+            self.phi1, self.phi2, n = device_derivatives(loss, t, F)
+            _count_clamps(loss, n, 2)
+            return
         m = to_host(tttp_affine(t, F, 1.0, 0.0, torch.float64))
         p1 = np.asarray(loss.dphi(t.values, m), dtype=np.float64)
         p2 = np.asarray(loss.d2phi(t.values, m), dtype=np.float64)
@@ -317,7 +323,12 @@ def gradient_blocks(t: SparseTensor, factors, loss: LossFunction, reg: float,
     """Per-mode gradient blocks: MTTKRP of the dphi tensor plus 2 reg A
     (optim.py:336-345)."""
     F = _factors_dev(factors)
-    if model is not None:
+    if model is not None and loss.device_id is not None and t.nnz:
+        from .losses import _count_clamps, _loss_eval
+        (_, phi1, _), n = _loss_eval(loss, t.device_values(_torch().float64),
+                                     model.device_values(_torch().float64), d1=True)
+        _count_clamps(loss, n, 1)
+    elif model is not None:
         p1 = np.asarray(loss.dphi(t.values, model.values), dtype=np.float64)
         phi1 = _dev(p1)
     else:

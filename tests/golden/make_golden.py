@@ -19,6 +19,10 @@ Fixtures:
   cfg1.npz           -- BASELINE cfg 1: tttp, mttkrp x3, 5 ALS sweeps (+rmse),
                         2 CCD++ sweeps, 3 SGD steps, all from the reference
   drivers_small.npz  -- ALS/CCD/SGD single sweeps and run() traces, small case
+  generalized.npz    -- Poisson log-link (and generalized least squares):
+                        derivative tensors / objective incl. exp clamp counts,
+                        inner-Newton ALS and CCD++ sweeps, SGD steps, run()
+                        traces
   second_order.npz   -- hessian_matvec (ls/poisson x gauss_newton/newton),
                         gradient_blocks, gn_step trajectories (ls GN, ls
                         Newton, poisson GN) and run(algorithm=gn/newton) traces
@@ -288,6 +292,65 @@ def second_order():
     np.savez_compressed(os.path.join(HERE, "second_order.npz"), **out)
 
 
+def generalized():
+    out = {}
+    t, truth = cpfit.gen_low_rank((14, 12, 10), 3, 0.5, rng=cpfit.RngState(41))
+    noise = np.random.default_rng(42)
+    counts = np.round(np.exp(np.clip(t.values, -3, 3)) + noise.random(t.nnz))
+    tp = t.with_values(counts)
+    out["dims"] = np.array(tp.shape)
+    out["keys"] = tp.keys
+    out["values"] = tp.values
+    init = [0.3 * f + 0.05 * noise.standard_normal(f.shape) for f in truth]
+    for n in range(3):
+        out[f"init{n}"] = init[n]
+    # elementwise: derivative tensors and objective, with clamped entries
+    loss = cpfit.get_loss("poisson")
+    big = [f.copy() for f in init]
+    big[0] = big[0] * 3000.0
+    model = cpfit.model_at_observed(tp.observation_mask(), big)
+    p1, p2 = cpfit.derivative_tensors(loss, tp, model)
+    out["big0"] = big[0]
+    out["clamp_phi1"] = p1.values
+    out["clamp_phi2"] = p2.values
+    out["clamp_count_derivs"] = np.array(loss.diagnostics["exp_clamped"])
+    out["clamp_obj"] = np.array(cpfit.objective(loss, tp, big, reg=1e-3))
+    out["clamp_count_total"] = np.array(loss.diagnostics["exp_clamped"])
+    # sweeps
+    for algo, nsweep, kw in (("als", 2, {}), ("als_frozen", 2, {"freeze_curvature": True}),
+                             ("ccd", 2, {}), ("sgd", 3, {"sample_rate": 0.5, "step": 1e-2})):
+        loss = cpfit.get_loss("poisson")
+        cfg = ro.SolverConfig(rank=3, reg=1e-3, loss="poisson", **kw)
+        state = ro.CompletionState(factors=[f.copy() for f in init], rng=cpfit.RngState(0))
+        for s in range(nsweep):
+            if algo.startswith("als"):
+                ro.als_sweep(tp, state, loss, cfg)
+            elif algo == "ccd":
+                ro.ccd_sweep(tp, state, loss, cfg)
+            else:
+                ro.sgd_sweep(tp, state, loss, cfg, cpfit.RngState(5).child(s))
+            for n in range(3):
+                out[f"{algo}{s}_f{n}"] = state.factors[n].copy()
+    # least squares through the generalized (inner Newton) ALS path
+    loss = cpfit.get_loss("ls")
+    cfg = ro.SolverConfig(rank=3, reg=1e-3)
+    state = ro.CompletionState(factors=[f.copy() for f in init], rng=cpfit.RngState(0))
+    ro.als_sweep(t, state, loss, cfg, generalized=True)
+    out["lsgen_values"] = t.values
+    for n in range(3):
+        out[f"lsgen_f{n}"] = state.factors[n].copy()
+    # run() traces
+    for algo in ("als", "ccd", "sgd"):
+        cfg = ro.SolverConfig(rank=3, algorithm=algo, loss="poisson", max_iters=3, seed=4,
+                              deterministic=True, record_every=1, sample_rate=0.5, step=1e-2)
+        trace, state = ro.run(tp, cfg, return_state=True)
+        out[f"run_{algo}_obj"] = np.array([r.objective for r in trace.records])
+        out[f"run_{algo}_metric"] = np.array([r.metric for r in trace.records])
+        for n in range(3):
+            out[f"run_{algo}_f{n}"] = state.factors[n]
+    np.savez_compressed(os.path.join(HERE, "generalized.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -298,6 +361,7 @@ if __name__ == "__main__":
     philox()
     cfg1()
     drivers_small()
+    generalized()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
