@@ -266,6 +266,21 @@ int cpfit_ccd_fold(cpfit_pattern *p, int mode, const double *const *sub,
 int cpfit_ccd_finalize(int64_t dim, const double *numden, double reg,
                        double *col, void *stream);
 
+/* ---- ingest -------------------------------------- */
+/* from_coords on the device (core.py:78-90, 208-231): coords[q] = n device
+ * coordinates of mode q (int32 if coord_bytes == 4, int64 if 8), vals = n
+ * fp64 values, any order, duplicates allowed.  Writes the strictly
+ * increasing unique linearized keys (row-major, last mode fastest) to
+ * keys_out and their values to vals_out (duplicates summed exactly as
+ * np.add.reduceat does in stable key order: bit-identical), *nnz_out = the
+ * unique count (both outputs need room for n).  A coordinate outside
+ * [0, dims[q]) returns CPFIT_EINVAL with *bad_mode = the lowest such mode
+ * (the reference's ValueError "coordinate out of range [0, d) in mode q"). */
+int cpfit_from_coords(int order, const int64_t *dims, int64_t n, int coord_bytes,
+                      const void *const *coords, const double *vals,
+                      uint64_t *keys_out, double *vals_out, int64_t *nnz_out,
+                      int *bad_mode, void *stream);
+
 /* ---- generalized losses (losses.py:22-104) ---------------------------- */
 /* Loss ids: 0 = least squares (phi = (t - m)^2, dphi = 2 (m - t), d2phi = 2),
  * 1 = Poisson log link (phi = exp(m~) - t m, dphi = exp(m~) - t, d2phi =

@@ -39,7 +39,7 @@ SYMBOLS = (
     "cpfit_ccd_fold", "cpfit_ccd_finalize", "cpfit_check_finite",
     "cpfit_tttp_host", "cpfit_tttp_subst", "cpfit_axpby", "cpfit_spd_inverse_rows",
     "cpfit_batched_symv", "cpfit_tttp_loss", "cpfit_loss_eval", "cpfit_ccd_gen_weights",
-    "cpfit_ccd_gen_update", "cpfit_ccd_gen_model",
+    "cpfit_ccd_gen_update", "cpfit_ccd_gen_model", "cpfit_from_coords",
 )
 
 _vp = ctypes.c_void_p
@@ -109,6 +109,8 @@ def load(path: str | None = None):
                                   ctypes.POINTER(_i64), _vp],
         "cpfit_ccd_gen_update": [_i64, _vp, _vp, ctypes.c_double, _vp, _vp, _vp],
         "cpfit_ccd_gen_model": [_vp, _int, _vp, _vp, _vp, _vp],
+        "cpfit_from_coords": [_int, ctypes.POINTER(_i64), _i64, _int, _PP, _vp, _vp, _vp,
+                              ctypes.POINTER(_i64), ctypes.POINTER(_int), _vp],
         "cpfit_ccd_fold": [_vp, _int, _PP, _PP, _vp, _vp],
         "cpfit_ccd_finalize": [_i64, _vp, ctypes.c_double, _vp, _vp],
         "cpfit_probe_gather": [_vp, _int, _int, _PP, _i64, _vp, _i64, _vp],

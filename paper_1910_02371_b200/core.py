@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _lib
 from .exceptions import DataError
-from .validation import check_mode, check_shape
+from .validation import _is_torch, check_mode, check_shape
 
 DEFAULT_CELL_CAP = 1 << 26
 
@@ -465,13 +465,75 @@ def build_tensor(entries, shape) -> SparseTensor:
 
 
 def from_coords(coord_arrays, values, shape) -> SparseTensor:
-    """core.py:208-218: per-mode coordinate arrays, duplicates summed."""
+    """core.py:208-218: per-mode coordinate arrays, duplicates summed.
+
+    With a CUDA device the whole ingest runs there (cpfit_from_coords:
+    linearize, stable radix sort, duplicate merge in numpy's reduceat order;
+    bit-identical keys and values); numpy inputs are uploaded first.  Without
+    one (CPU-only host-logic tests) the numpy restatement below is used."""
     shape = check_shape(shape)
+    if len(coord_arrays) != len(shape):
+        raise ValueError("one coordinate array per mode required")
+    torch = _torch()
+    if torch.cuda.is_available():
+        return from_coords_device(coord_arrays, values, shape)
     values = np.ascontiguousarray(values, dtype=np.float64)
     keys = linearize_many(coord_arrays, shape)
     if keys.shape != values.shape:
         raise ValueError("coordinate arrays and values must have equal length")
     return _merge_sorted(shape, keys, values)
+
+
+def from_coords_device(coord_arrays, values, shape) -> SparseTensor:
+    """from_coords on the device: coordinate arrays (int32 / int64, numpy or
+    CUDA tensors, any order, duplicates allowed) and fp64 values -> a tensor
+    whose sorted keys and merged values stay on the device."""
+    torch = _torch()
+    shape = check_shape(shape)
+    if len(coord_arrays) != len(shape):
+        raise ValueError("one coordinate array per mode required")
+    dev = cuda_device()
+
+    if _is_torch(values):
+        vals = values.to(device=dev, dtype=torch.float64).contiguous().reshape(-1)
+    else:
+        vals = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64).reshape(-1)).to(dev)
+    cs = []
+    for q, c in enumerate(coord_arrays):
+        if _is_torch(c):
+            ct = c.to(dev)
+            if ct.dtype not in (torch.int32, torch.int64):
+                ct = ct.to(torch.int64)
+        else:
+            a = np.asarray(c)
+            if a.dtype != np.int32:
+                if a.size and a.dtype.kind == "u" and int(a.max()) > np.iinfo(np.int64).max:
+                    raise ValueError(f"coordinate out of range [0, {shape[q]}) in mode {q}")
+                a = a.astype(np.int64)
+            ct = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        cs.append(ct.contiguous().reshape(-1))
+    width = 4 if all(c.dtype == torch.int32 for c in cs) else 8
+    if width == 8:
+        cs = [c.to(torch.int64) for c in cs]
+    n = int(vals.numel())
+    if any(int(c.numel()) != n for c in cs):
+        raise ValueError("coordinate arrays and values must have equal length")
+    keys = torch.empty(n, dtype=torch.int64, device=dev)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    nnz = ctypes.c_int64(0)
+    bad = ctypes.c_int(-1)
+    dims = (ctypes.c_int64 * len(shape))(*shape)
+    arr = _lib.ptr_array([c.data_ptr() for c in cs])
+    st = _lib.load().cpfit_from_coords(
+        len(shape), dims, n, width, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)),
+        ctypes.c_void_p(vals.data_ptr()), ctypes.c_void_p(keys.data_ptr()),
+        ctypes.c_void_p(out.data_ptr()), ctypes.byref(nnz), ctypes.byref(bad),
+        ctypes.c_void_p(current_stream()))
+    if st != 0 and bad.value >= 0:
+        raise ValueError(f"coordinate out of range [0, {shape[bad.value]}) in mode {bad.value}")
+    _lib.check(st, "from_coords")
+    m = nnz.value
+    return SparseTensor.from_device(shape, keys[:m], out[:m])
 
 
 def _merge_sorted(shape, keys, values) -> SparseTensor:

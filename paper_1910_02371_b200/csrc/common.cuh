@@ -169,6 +169,14 @@ struct CpfitCols {
   const int32_t *idx[CPFIT_MAXN];
 };
 
+struct CpfitDims {
+  int64_t d[CPFIT_MAXN];
+};
+template <typename C>
+struct CpfitCoordPtrs {
+  const C *p[CPFIT_MAXN];
+};
+
 // ---- elementwise losses (losses.py:41-91) -----------------------------------
 // loss 0: least squares  phi = (t - m)^2, dphi = 2 (m - t), d2phi = 2
 // loss 1: Poisson log link  phi = exp(m~) - t m, dphi = exp(m~) - t,
@@ -196,6 +204,11 @@ __device__ __forceinline__ bool loss_eval1(int loss, double t, double m, double 
 // out[i] = sum_{j<i} in[j] for i in [0, n]; out has n+1 entries (out[n] = total).
 template <typename Tin>
 int exclusive_scan(const Tin *in, int64_t *out, int64_t n, cudaStream_t s);
+
+// stable LSD radix sort of positions by the low `bits` bits of uint64 keys
+template <typename K>
+int radix_sort_pairs(const K *keys, int64_t n, int bits, K *sorted_keys, int32_t *perm,
+                     cudaStream_t s);
 
 // gather: out[k] = in[idx[k]]
 int gather_i32(const int32_t *in, const int32_t *idx, int32_t *out, int64_t n,

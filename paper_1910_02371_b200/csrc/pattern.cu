@@ -10,6 +10,8 @@
 #include <new>
 #include <vector>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace cpfit {
@@ -251,8 +253,14 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ITEMS = 8;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 
+template <typename K>
+__device__ __forceinline__ int radix_digit(K key, int shift) {
+  return (int)((((typename std::make_unsigned<K>::type)key) >> shift) & 255u);
+}
+
+template <typename K>
 __global__ void __launch_bounds__(RS_THREADS)
-radix_upsweep(const int32_t *__restrict__ keys, int64_t n, int shift, int64_t nblocks,
+radix_upsweep(const K *__restrict__ keys, int64_t n, int shift, int64_t nblocks,
               int32_t *__restrict__ counts) {
   __shared__ int hist[256];
   for (int i = threadIdx.x; i < 256; i += RS_THREADS) hist[i] = 0;
@@ -260,7 +268,7 @@ radix_upsweep(const int32_t *__restrict__ keys, int64_t n, int shift, int64_t nb
   int64_t base = (int64_t)blockIdx.x * RS_TILE;
   for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) {
     int64_t k = base + i;
-    if (k < n) atomicAdd(&hist[((uint32_t)keys[k] >> shift) & 255u], 1);
+    if (k < n) atomicAdd(&hist[radix_digit(keys[k], shift)], 1);
   }
   __syncthreads();
   for (int d = threadIdx.x; d < 256; d += RS_THREADS)
@@ -268,16 +276,18 @@ radix_upsweep(const int32_t *__restrict__ keys, int64_t n, int shift, int64_t nb
 }
 
 // vals_in == nullptr means the identity (first pass).
+template <typename K>
 __global__ void __launch_bounds__(RS_THREADS)
-radix_downsweep(const int32_t *__restrict__ keys_in, const int32_t *__restrict__ vals_in,
+radix_downsweep(const K *__restrict__ keys_in, const int32_t *__restrict__ vals_in,
                 int64_t n, int shift, int64_t nblocks, const int64_t *__restrict__ offs,
-                int32_t *__restrict__ keys_out, int32_t *__restrict__ vals_out) {
+                K *__restrict__ keys_out, int32_t *__restrict__ vals_out) {
   __shared__ int whist[RS_WARPS][257];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = lane; i < 257; i += 32) whist[w][i] = 0;
   __syncwarp();
   const int64_t wbase = (int64_t)blockIdx.x * RS_TILE + (int64_t)w * 32 * RS_ITEMS;
-  int32_t key[RS_ITEMS], rank[RS_ITEMS];
+  K key[RS_ITEMS];
+  int32_t rank[RS_ITEMS];
   int digit[RS_ITEMS];
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
@@ -285,7 +295,7 @@ radix_downsweep(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
     int64_t k = wbase + j * 32 + lane;
     bool valid = k < n;
     key[j] = valid ? keys_in[k] : 0;
-    int d = valid ? (int)(((uint32_t)key[j] >> shift) & 255u) : 256;
+    int d = valid ? radix_digit(key[j], shift) : 256;
     digit[j] = d;
     unsigned peers = __match_any_sync(0xffffffffu, d);
     int pre = whist[w][d];
@@ -319,49 +329,63 @@ radix_downsweep(const int32_t *__restrict__ keys_in, const int32_t *__restrict__
   }
 }
 
-// Stable sort of positions 0..n-1 by keys (non-negative, < dim).
-// Writes sorted keys and the permutation.
-static int radix_sort_positions(const int32_t *keys, int64_t n, int64_t dim,
-                                int32_t *sorted_keys, int32_t *perm, cudaStream_t s) {
-  int bits = 0;
-  while (bits < 31 && ((int64_t)1 << bits) < dim) ++bits;
+// Stable LSD sort of positions 0..n-1 by the low `bits` bits of keys
+// (int32 mode coordinates or uint64 linearized keys).  Writes the sorted keys
+// and the permutation.
+template <typename K>
+int radix_sort_pairs(const K *keys, int64_t n, int bits, K *sorted_keys, int32_t *perm,
+                     cudaStream_t s) {
   int passes = (bits + 7) / 8;
   if (passes == 0 || n <= 1) {
     iota_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(perm, n);
     CPFIT_LAUNCH_CHECK("iota");
-    if (n) CPFIT_CUDA(cudaMemcpyAsync(sorted_keys, keys, n * sizeof(int32_t),
+    if (n) CPFIT_CUDA(cudaMemcpyAsync(sorted_keys, keys, n * sizeof(K),
                                       cudaMemcpyDeviceToDevice, s));
     return CPFIT_OK;
   }
   int64_t nblocks = (n + RS_TILE - 1) / RS_TILE;
-  Scratch<int32_t> counts(s), k_tmp(s), v_tmp(s);
+  Scratch<int32_t> counts(s), v_tmp(s);
+  Scratch<K> k_tmp(s);
   Scratch<int64_t> offs(s);
   CPFIT_TRY(counts.alloc(256 * nblocks));
   CPFIT_TRY(offs.alloc(256 * nblocks + 1));
   CPFIT_TRY(k_tmp.alloc(n));
   CPFIT_TRY(v_tmp.alloc(n));
   // ping-pong so that the last pass lands in (sorted_keys, perm)
-  int32_t *kb[2], *vb[2];
+  K *kb[2];
+  int32_t *vb[2];
   if (passes % 2 == 1) {
     kb[0] = sorted_keys; vb[0] = perm; kb[1] = k_tmp.ptr; vb[1] = v_tmp.ptr;
   } else {
     kb[0] = k_tmp.ptr; vb[0] = v_tmp.ptr; kb[1] = sorted_keys; vb[1] = perm;
   }
-  const int32_t *kin = keys;
+  const K *kin = keys;
   const int32_t *vin = nullptr;
   for (int p = 0; p < passes; ++p) {
     int shift = 8 * p;
-    radix_upsweep<<<(unsigned)nblocks, RS_THREADS, 0, s>>>(kin, n, shift, nblocks, counts.ptr);
+    radix_upsweep<K><<<(unsigned)nblocks, RS_THREADS, 0, s>>>(kin, n, shift, nblocks,
+                                                              counts.ptr);
     CPFIT_LAUNCH_CHECK("radix_upsweep");
     CPFIT_TRY(exclusive_scan<int32_t>(counts.ptr, offs.ptr, 256 * nblocks, s));
-    int32_t *ko = kb[p % 2], *vo = vb[p % 2];
-    radix_downsweep<<<(unsigned)nblocks, RS_THREADS, 0, s>>>(kin, vin, n, shift, nblocks,
-                                                             offs.ptr, ko, vo);
+    K *ko = kb[p % 2];
+    int32_t *vo = vb[p % 2];
+    radix_downsweep<K><<<(unsigned)nblocks, RS_THREADS, 0, s>>>(kin, vin, n, shift, nblocks,
+                                                                offs.ptr, ko, vo);
     CPFIT_LAUNCH_CHECK("radix_downsweep");
     kin = ko;
     vin = vo;
   }
   return CPFIT_OK;
+}
+template int radix_sort_pairs<uint64_t>(const uint64_t *, int64_t, int, uint64_t *, int32_t *,
+                                        cudaStream_t);
+
+// Stable sort of positions 0..n-1 by keys (non-negative, < dim).
+static int radix_sort_positions(const int32_t *keys, int64_t n, int64_t dim,
+                                int32_t *sorted_keys, int32_t *perm, cudaStream_t s) {
+  int bits = 0;
+  while (bits < 31 && ((int64_t)1 << bits) < dim) ++bits;
+  return radix_sort_pairs<int32_t>(keys, n, bits, sorted_keys, perm, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -23,6 +23,10 @@ Fixtures:
                         derivative tensors / objective incl. exp clamp counts,
                         inner-Newton ALS and CCD++ sweeps, SGD steps, run()
                         traces
+  ingest.npz         -- from_coords with heavy duplicates (segments < 8,
+                        8..128 and > 128 long: numpy's reduceat/pairwise
+                        order), order-4 int32 coordinates, and parse_tns of a
+                        generated .tns text
   second_order.npz   -- hessian_matvec (ls/poisson x gauss_newton/newton),
                         gradient_blocks, gn_step trajectories (ls GN, ls
                         Newton, poisson GN) and run(algorithm=gn/newton) traces
@@ -351,6 +355,55 @@ def generalized():
     np.savez_compressed(os.path.join(HERE, "generalized.npz"), **out)
 
 
+def ingest():
+    from cpfit import tensor_io as rio
+    rng = np.random.default_rng(51)
+    out = {}
+    shape = (50, 40, 30)
+    n = 80_000
+    c = [rng.integers(0, d, n).astype(np.int32) for d in shape]
+    for q, v in enumerate((7, 11, 13)):
+        c[q][:3000] = v          # one key 3000 times (recursive pairwise halves)
+    for q, v in enumerate((1, 2, 3)):
+        c[q][3000:3100] = v      # one key 100 times (eight accumulators)
+    vals = rng.standard_normal(n) * 10.0 ** rng.integers(-6, 7, n)
+    perm = rng.permutation(n)
+    c = [x[perm] for x in c]
+    vals = vals[perm]
+    t = cpfit.from_coords(c, vals, shape)
+    out["a_shape"] = np.array(shape)
+    for q in range(3):
+        out[f"a_c{q}"] = c[q]
+    out["a_vals"] = vals
+    out["a_keys"] = t.keys
+    out["a_out"] = t.values
+    shape4 = (100_000, 100_000, 100_000, 1000)
+    m = 40_000
+    c4 = [rng.integers(0, d, m).astype(np.int32) for d in shape4]
+    v4 = rng.standard_normal(m)
+    t4 = cpfit.from_coords(c4, v4, shape4)
+    out["b_shape"] = np.array(shape4)
+    for q in range(4):
+        out[f"b_c{q}"] = c4[q]
+    out["b_vals"] = v4
+    out["b_keys"] = t4.keys
+    out["b_out"] = t4.values
+    lines = ["# a comment", "# dims: 9 8 7"]
+    for _ in range(400):
+        i, j, k = (int(rng.integers(1, 10)), int(rng.integers(1, 9)), int(rng.integers(1, 8)))
+        lines.append(f"{i} {j} {k} {rng.standard_normal()!r}")
+    text = "\n".join(lines) + "\n"
+    path = "/tmp/cpfit_golden.tns"
+    with open(path, "w") as fh:
+        fh.write(text)
+    tt = rio.parse_tns(path)
+    out["tns_text"] = np.array(text)
+    out["tns_shape"] = np.array(tt.shape)
+    out["tns_keys"] = tt.keys
+    out["tns_vals"] = tt.values
+    np.savez_compressed(os.path.join(HERE, "ingest.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -362,6 +415,7 @@ if __name__ == "__main__":
     cfg1()
     drivers_small()
     generalized()
+    ingest()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
