@@ -446,12 +446,17 @@ __device__ __forceinline__ void solve_empty_row(const SolveParams<T> &p, int64_t
 }
 
 // Register-resident warp Cholesky solve for R <= RMAX <= 32.  Lane j holds
-// column j of (G + reg I) in a[] (G is stored symmetric, so column j = row j,
-// a contiguous load); b[] (right-hand side, then y, then x) is replicated in
-// every lane.  Step k broadcasts column k of L (one shuffle per element), which
-// every lane also uses for the forward substitution; lanes right of k apply
-// the trailing update to their own column.  Back substitution: lane k owns
-// L[:, k], so x_k needs one dot product on lane k and one broadcast.
+// column j of (G + reg I) in a[] (G is symmetric: column j is loaded as row
+// entries G[i][j] -- coalesced across lanes) and b_j of the right-hand side
+// (then y_j, then x_j).  Step k broadcasts the UNSCALED column k (one shuffle
+// per element); the scaling by 1/L[k][k] is folded into the per-lane scalar
+// s_j = A[j][k] / d of the trailing update, so each element costs two
+// shuffles and one FMA.  Column j stays unscaled on lane j, and lane j's own
+// a[k] is A[j][k] -- row j of L times L[k][k] -- so the forward and back
+// substitutions need one broadcast and one FMA per step:
+//   y_k = b_k / L_kk,  b_j -= (A[j][k] / L_kk) y_k            (j > k)
+//   x_k = z_k / L_kk,  z_j -= (A[k][j] / L_jj) x_k            (j < k)
+// Registers: the column (2 R) and a handful of scalars.
 template <typename T, int RMAX>
 __device__ __forceinline__ void chol_factor_solve(const T *__restrict__ Gr,
                                                   const T *__restrict__ rh, int R, double reg,
@@ -460,54 +465,42 @@ __device__ __forceinline__ void chol_factor_solve(const T *__restrict__ Gr,
   // identity (block diagonal: same solution), so every loop below is
   // guard-free and every shuffle is warp-uniform.
   const int lane = threadIdx.x & 31;
-  double a[RMAX], b[RMAX];
+  double a[RMAX];
 #pragma unroll
   for (int i = 0; i < RMAX; ++i) {
     const bool in = i < R && lane < R;
-    a[i] = in ? (double)__ldg(Gr + lane * R + i) + (i == lane ? reg : 0.0)
+    a[i] = in ? (double)__ldg(Gr + i * R + lane) + (i == lane ? reg : 0.0)
               : (i == lane ? 1.0 : 0.0);
-    b[i] = i < R ? (double)__ldg(rh + i) : 0.0;
   }
+  double bj = lane < R ? (double)__ldg(rh + lane) : 0.0;
   bool ok = true;
   double my_inv = 1.0;  // 1 / L[lane][lane]
 #pragma unroll
   for (int k = 0; k < RMAX; ++k) {
     const double d = __shfl_sync(0xffffffffu, a[k], k);
     ok = ok && (d > 0.0) && (d < DBL_MAX);
-    const double lkk = sqrt(d);
-    const double inv = 1.0 / lkk;
-    const double yk = b[k] * inv;
-    double ljk = 0.0;
+    const double inv = 1.0 / sqrt(d);
+    const double yk = __shfl_sync(0xffffffffu, bj, k) * inv;
+    const bool right = lane > k;
+    const double ljk = a[k] * inv;                      // L[j][k] on lanes j > k
+    const double sj = right ? ljk * inv : 0.0;          // A[j][k] / d
+    bj = right ? fma(-ljk, yk, bj) : (lane == k ? yk : bj);
+    if (lane == k) my_inv = inv;
 #pragma unroll
     for (int i = k + 1; i < RMAX; ++i) {
-      const double ci = __shfl_sync(0xffffffffu, a[i], k) * inv;  // L[i][k]
-      ljk = (i == lane) ? ci : ljk;                              // L[lane][k] once i == lane
-      a[i] = fma(-ci, ljk, a[i]);  // trailing update (no-op while ljk == 0)
-      b[i] = fma(-ci, yk, b[i]);   // forward substitution, replicated in every lane
+      const double ci = __shfl_sync(0xffffffffu, a[i], k);  // A[i][k] (unscaled)
+      a[i] = fma(-ci, sj, a[i]);  // trailing update of column lane
     }
-    const double m = lane == k ? inv : 1.0;  // lane k: column k becomes L[:, k]
-#pragma unroll
-    for (int i = k + 1; i < RMAX; ++i) a[i] *= m;
-    if (lane == k) {
-      a[k] = lkk;
-      my_inv = inv;
-    }
-    b[k] = yk;
   }
-  // back substitution L^T x = y: lane k owns L[:, k] (garbage when !ok, not stored)
+  // back substitution L^T x = y (garbage when !ok, not stored)
 #pragma unroll
   for (int kk = 0; kk < RMAX; ++kk) {
     const int k = RMAX - 1 - kk;
-    double sdot = 0.0;
-#pragma unroll
-    for (int i = k + 1; i < RMAX; ++i) sdot = fma(a[i], b[i], sdot);
-    b[k] = __shfl_sync(0xffffffffu, (b[k] - sdot) * my_inv, k);
+    const double xk = __shfl_sync(0xffffffffu, bj * my_inv, k);
+    if (lane == k) bj = xk;
+    if (lane < k) bj = fma(-(a[k] * my_inv), xk, bj);
   }
-  double mine = 0.0;
-#pragma unroll
-  for (int i = 0; i < RMAX; ++i)
-    if (i == lane) mine = b[i];
-  mine_out = mine;
+  mine_out = bj;
   ok_out = __all_sync(0xffffffffu, ok);
 }
 
