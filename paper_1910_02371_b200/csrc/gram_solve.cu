@@ -62,7 +62,10 @@ constexpr int GRAM_CHUNK = 32;  // Hadamard rows staged per MMA sweep
 
 template <int RT>
 constexpr int gram_ld() {
-  return RT * 8 + 8;  // +8 doubles: rows 64 B apart in bank space
+  // +4 doubles: consecutive rows 32 B (8 banks) apart, so the four rows an
+  // MMA operand load touches per half-warp (lane = 4 gq + tq reads row tq,
+  // column gq) land on disjoint banks (+8 gave 2-way conflicts)
+  return RT * 8 + 4;
 }
 
 constexpr int pow2_at_least(int x) {
