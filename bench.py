@@ -330,6 +330,24 @@ def als_section(world, rank, dev, sweeps=3):
         out["gn_step_cg_iters"] = cg
         out["gn_step_note"] = ("one damped Gauss-Newton step (gn_damping=1, cg_tol 5e-3, "
                                "cg_max min(30, 3R)) after one ALS sweep from the default init")
+        # generalized loss: one inner-Newton ALS sweep of the
+        # Poisson log link on the same counts, everything on the device
+        from paper_1910_02371_b200.optim import _als_generalized_device
+        pcfg = SolverConfig(rank=R3, reg=REG, loss="poisson")
+        ploss = get_loss("poisson")
+        Fp = [f.clone() for f in init]
+        _als_generalized_device(t, Fp, ploss, pcfg)  # warm-up
+        Fp = [f.clone() for f in init]
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _als_generalized_device(t, Fp, ploss, pcfg)
+        b.record(stream)
+        torch.cuda.synchronize()
+        out["poisson_als_sweep_ms"] = a.elapsed_time(b)
+        out["poisson_als_note"] = ("inner-Newton ALS sweep, Poisson log link (inner_max 5, "
+                                   "inner_tol 1e-3): fused TTTP loss epilogue + MTTKRP + "
+                                   "phi2-weighted Gram + batched solve per inner step")
     else:
         from paper_1910_02371_b200 import dist as D
         coords = []
@@ -458,6 +476,51 @@ def sgd_section(dev, steps=5, world=1):
                                      "sgd_step_s": CPU_CFG5_SCALED["sgd_step_s_at_1e7"] * 100,
                                      "note": "reference f64 numpy path at 1e7 nnz x 100 "
                                              "(1e9 does not fit the reference host; SURVEY 8d)"}}
+
+
+def ingest_section(dev, reps=3):
+    """from_coords on the device at the cfg 2 size --
+    1.1e7 coordinate triples (1e7 distinct keys plus 10% duplicates, shuffled)
+    -> sorted unique keys + merged values, bit-identical to the reference's
+    numpy path; the numpy restatement of core.py:208-231 (linearize_many,
+    stable argsort, np.add.reduceat) timed beside it on the host."""
+    import torch
+
+    from paper_1910_02371_b200 import synth
+    from paper_1910_02371_b200.core import _merge_sorted, from_coords_device, linearize_many
+    shape, keys, values, _ = synth.cfg2()
+    rng = np.random.default_rng(77)
+    dup = rng.integers(0, keys.size, keys.size // 10)
+    allk = np.concatenate([keys, keys[dup]])
+    allv = np.concatenate([values, rng.standard_normal(dup.size)])
+    order = rng.permutation(allk.size)
+    allk, allv = allk[order], allv[order]
+    coords = synth._delinearize(allk, shape)
+    dc = [torch.from_numpy(np.ascontiguousarray(c, dtype=np.int32)).to(dev) for c in coords]
+    dv = torch.from_numpy(allv).to(dev)
+    out = {"workload": f"cfg 2 shape, {allk.size} coordinate triples (int32, shuffled, "
+                       f"{dup.size} duplicates) -> {keys.size} unique keys",
+           "entries": int(allk.size)}
+    t = from_coords_device(dc, dv, shape)  # warm-up (allocator, module load)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        t = from_coords_device(dc, dv, shape)
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    out["device_ms"] = float(np.median(times))
+    out["device_entries_per_s"] = allk.size / (out["device_ms"] * 1e-3)
+    t0 = time.perf_counter()
+    ref = _merge_sorted(shape, linearize_many(coords, shape), allv)
+    out["host_numpy_s"] = time.perf_counter() - t0
+    out["host_what"] = "numpy restatement of core.py:208-231 on one host core"
+    ok = t.nnz == ref.nnz and np.array_equal(t.keys, ref.keys) and \
+        np.array_equal(t.values, ref.values)
+    out["bit_identical_to_numpy"] = bool(ok)
+    return out
 
 
 def dense_section(dev, sweeps=2):
@@ -733,6 +796,13 @@ def main():
         except Exception as exc:
             als = {"error": repr(exc)}
         torch.cuda.empty_cache()
+    ingest = None
+    if world == 1:
+        try:
+            ingest = ingest_section(dev)
+        except Exception as exc:
+            ingest = {"error": repr(exc)}
+        torch.cuda.empty_cache()
     dense = None
     if not args.no_dense and world == 1:
         try:
@@ -750,7 +820,7 @@ def main():
             "roofline": roofline, "kernels": kernels, "gather_ceiling": probe,
             "compulsory_bytes_per_pass": compulsory,
             "clocks": clk, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
-            "als": als, "dense": dense, "sgd": sgd,
+            "als": als, "dense": dense, "sgd": sgd, "ingest": ingest,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample()
