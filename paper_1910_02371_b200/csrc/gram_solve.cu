@@ -258,6 +258,161 @@ gram_kernel(const GramParams<T> p) {
   }
 }
 
+// Register-fragment Gram kernel (fp64, fixed number of other modes, R <= 32):
+// no shared-memory staging.  The DMMA m8n8k4 operand of lane (gq, tq) for
+// column block i and k-step kk is H[kk + tq][8 i + gq] -- one element of the
+// Hadamard row of entry kk + tq -- so every lane gathers exactly the factor
+// elements its own fragments need (8 lanes with the same tq read 64
+// contiguous bytes of one row) and multiplies them in registers.  Stream and
+// gather loads run one stage (U k-steps) ahead of the MMAs, indices two
+// stages ahead, so each warp overlaps its own gather latency with its tensor
+// work.  Tile set as gram_kernel (upper-triangular 8x8 tiles); the per-tile
+// accumulation order over k is the same, so results agree with gram_kernel
+// to rounding of the (identical) products.
+#ifndef CPFIT_GRAM_FRAG_U
+#define CPFIT_GRAM_FRAG_U 2
+#endif
+constexpr int GRAM_FRAG_WARPS = 4;
+
+template <int RT, int NPT, int U>
+struct GramFragStage {
+  double x[U][NPT][RT];
+  double sw[U], tv[U];
+};
+
+template <int RT, int NPT, int U>
+__device__ __forceinline__ void gram_frag_idx(const GramParams<double> &p, int64_t kb,
+                                              int64_t b1, int tq, int32_t (&ix)[U][NPT]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t e = kb + 4 * u + tq;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) ix[u][n] = e < b1 ? __ldg(p.idx[n] + e) : -1;
+  }
+}
+
+template <int RT, int NPT, int U>
+__device__ __forceinline__ void gram_frag_load(const GramParams<double> &p, int64_t kb,
+                                               int64_t b1, int gq, int tq,
+                                               const int32_t (&ix)[U][NPT],
+                                               GramFragStage<RT, NPT, U> &st) {
+  const int rank = p.rank;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t e = kb + 4 * u + tq;
+    const bool ok = e < b1;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+      const double *row = p.fac[n] + (size_t)(unsigned)(ok ? ix[u][n] : 0) * (unsigned)rank;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int col = 8 * i + gq;
+        st.x[u][n][i] = (ok && col < rank) ? __ldg(row + col) : 0.0;
+      }
+    }
+    double sw = 0.0, tv = 0.0;
+    if (ok) {
+      sw = 1.0;
+      if (p.weights) sw = sqrt(p.wperm ? __ldg(p.weights + __ldg(p.wperm + e)) : __ldg(p.weights + e));
+      if (p.vals) tv = p.vperm ? __ldg(p.vals + __ldg(p.vperm + e)) : __ldg(p.vals + e);
+    }
+    st.sw[u] = sw;
+    st.tv[u] = tv;
+  }
+}
+
+template <int RT, int NPT, int U>
+__global__ void __launch_bounds__(GRAM_FRAG_WARPS * 32)
+gram_frag_kernel(const GramParams<double> p) {
+  constexpr int NT = RT * (RT + 1) / 2;
+  constexpr int KS = 4 * U;  // entries per stage
+  const int lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int rank = p.rank;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < p.ntasks; t += nwarps) {
+    const int64_t b0 = p.task_begin[t], b1 = p.task_begin[t + 1];
+    double acc[NT][2];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = 0.0;
+    double racc[RT];
+#pragma unroll
+    for (int i = 0; i < RT; ++i) racc[i] = 0.0;
+    int32_t ix_next[U][NPT];
+    GramFragStage<RT, NPT, U> cur;
+    {
+      int32_t ix0[U][NPT];
+      gram_frag_idx<RT, NPT, U>(p, b0, b1, tq, ix0);
+      gram_frag_idx<RT, NPT, U>(p, b0 + KS, b1, tq, ix_next);
+      gram_frag_load<RT, NPT, U>(p, b0, b1, gq, tq, ix0, cur);
+    }
+    for (int64_t kb = b0; kb < b1; kb += KS) {
+      // next stage's gathers (indices loaded one stage earlier) and the
+      // indices of the stage after it are issued before this stage's MMAs
+      GramFragStage<RT, NPT, U> nxt;
+      gram_frag_load<RT, NPT, U>(p, kb + KS, b1, gq, tq, ix_next, nxt);
+      gram_frag_idx<RT, NPT, U>(p, kb + 2 * KS, b1, tq, ix_next);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        double f[RT];
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          double prod = cur.x[u][0][i];
+#pragma unroll
+          for (int n = 1; n < NPT; ++n) prod *= cur.x[u][n][i];
+          f[i] = prod * cur.sw[u];
+          racc[i] = fma(cur.tv[u], prod, racc[i]);
+        }
+        if (kb + 4 * u < b1) {
+          int tile = 0;
+#pragma unroll
+          for (int i = 0; i < RT; ++i)
+#pragma unroll
+            for (int jt = i; jt < RT; ++jt) {
+              dmma_8x8x4(acc[tile][0], acc[tile][1], f[i], f[jt]);
+              ++tile;
+            }
+        }
+      }
+      cur = nxt;
+    }
+    const int slot = p.task_slot[t];
+    double *dst = slot < 0 ? p.gram + (int64_t)p.task_row[t] * rank * rank
+                           : p.partial + (int64_t)slot * p.pstride;
+    if (p.vals) {
+      // entries of this task were split over tq: fixed xor tree over tq
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        racc[i] += __shfl_xor_sync(0xffffffffu, racc[i], 1);
+        racc[i] += __shfl_xor_sync(0xffffffffu, racc[i], 2);
+      }
+      double *rdst = slot < 0 ? p.rhs + (int64_t)p.task_row[t] * rank : dst + rank * rank;
+      if (tq == 0) {
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+          if (8 * i + gq < rank) rdst[8 * i + gq] = racc[i];
+      }
+    }
+    // accumulator fragment (tile (i, jt), element v) = G[8 i + gq][8 jt + 2 tq + v]
+    int tile = 0;
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int jt = i; jt < RT; ++jt) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int r = 8 * i + gq, c = 8 * jt + 2 * tq + v;
+          if (r < rank && c < rank) {
+            dst[(int64_t)r * rank + c] = acc[tile][v];
+            if (i != jt) dst[(int64_t)c * rank + r] = acc[tile][v];
+          }
+        }
+        ++tile;
+      }
+  }
+}
+
 template <typename T>
 __global__ void combine_gram_partials(const int32_t *__restrict__ split_row,
                                       const int32_t *__restrict__ split_slot, int64_t nsplit,
@@ -286,8 +441,38 @@ __global__ void check_weights_kernel(const T *__restrict__ w, int64_t n, int *fl
   if (bad && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+template <int RT, int NPT>
+static int launch_gram_frag(const GramParams<double> &p, cudaStream_t s) {
+  constexpr int U = CPFIT_GRAM_FRAG_U;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gram_frag_kernel<RT, NPT, U>,
+                                                  GRAM_FRAG_WARPS * 32, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int64_t blocks = (p.ntasks + GRAM_FRAG_WARPS - 1) / GRAM_FRAG_WARPS;
+  int64_t cap = (int64_t)num_sms() * per_sm;
+  unsigned grid = (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+  gram_frag_kernel<RT, NPT, U><<<grid, GRAM_FRAG_WARPS * 32, 0, s>>>(p);
+  CPFIT_LAUNCH_CHECK("gram_frag_kernel");
+  return CPFIT_OK;
+}
+
+static bool gram_frag_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *env = getenv("CPFIT_GRAM_FRAG");
+    on = env ? atoi(env) : 1;
+  }
+  return on != 0;
+}
+
 template <typename T, int RT, int VEC, int NPT>
 static int launch_gram_v(const GramParams<T> &p, cudaStream_t s) {
+  if constexpr (sizeof(T) == 8 && (NPT == 2 || NPT == 3) && RT <= 4) {
+    if (gram_frag_enabled())
+      return launch_gram_frag<RT, NPT>(reinterpret_cast<const GramParams<double> &>(p), s);
+  }
   constexpr int LD = gram_ld<RT>();
   const size_t smem = (size_t)GRAM_WARPS * GRAM_CHUNK * LD * sizeof(double);
   static bool configured = false;
