@@ -272,6 +272,12 @@ gram_kernel(const GramParams<T> p) {
 #ifndef CPFIT_GRAM_FRAG_U
 #define CPFIT_GRAM_FRAG_U 2
 #endif
+#ifndef CPFIT_GRAM_FRAG_NACC
+#define CPFIT_GRAM_FRAG_NACC 1
+#endif
+#ifndef CPFIT_GRAM_FRAG_MINB
+#define CPFIT_GRAM_FRAG_MINB 1
+#endif
 constexpr int GRAM_FRAG_WARPS = 4;
 
 template <int RT, int NPT, int U>
@@ -322,7 +328,7 @@ __device__ __forceinline__ void gram_frag_load(const GramParams<double> &p, int6
 }
 
 template <int RT, int NPT, int U>
-__global__ void __launch_bounds__(GRAM_FRAG_WARPS * 32)
+__global__ void __launch_bounds__(GRAM_FRAG_WARPS * 32, CPFIT_GRAM_FRAG_MINB)
 gram_frag_kernel(const GramParams<double> p) {
   constexpr int NT = RT * (RT + 1) / 2;
   constexpr int KS = 4 * U;  // entries per stage
@@ -333,9 +339,12 @@ gram_frag_kernel(const GramParams<double> p) {
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t t = warp; t < p.ntasks; t += nwarps) {
     const int64_t b0 = p.task_begin[t], b1 = p.task_begin[t + 1];
-    double acc[NT][2];
+    constexpr int NA = CPFIT_GRAM_FRAG_NACC;  // independent accumulator chains
+    double acc[NA][NT][2];
 #pragma unroll
-    for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int i = 0; i < NT; ++i) acc[a][i][0] = acc[a][i][1] = 0.0;
     double racc[RT];
 #pragma unroll
     for (int i = 0; i < RT; ++i) racc[i] = 0.0;
@@ -370,7 +379,7 @@ gram_frag_kernel(const GramParams<double> p) {
           for (int i = 0; i < RT; ++i)
 #pragma unroll
             for (int jt = i; jt < RT; ++jt) {
-              dmma_8x8x4(acc[tile][0], acc[tile][1], f[i], f[jt]);
+              dmma_8x8x4(acc[u % NA][tile][0], acc[u % NA][tile][1], f[i], f[jt]);
               ++tile;
             }
         }
@@ -394,6 +403,13 @@ gram_frag_kernel(const GramParams<double> p) {
           if (8 * i + gq < rank) rdst[8 * i + gq] = racc[i];
       }
     }
+#pragma unroll
+    for (int a = 1; a < NA; ++a)
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        acc[0][i][0] += acc[a][i][0];
+        acc[0][i][1] += acc[a][i][1];
+      }
     // accumulator fragment (tile (i, jt), element v) = G[8 i + gq][8 jt + 2 tq + v]
     int tile = 0;
 #pragma unroll
@@ -404,8 +420,8 @@ gram_frag_kernel(const GramParams<double> p) {
         for (int v = 0; v < 2; ++v) {
           const int r = 8 * i + gq, c = 8 * jt + 2 * tq + v;
           if (r < rank && c < rank) {
-            dst[(int64_t)r * rank + c] = acc[tile][v];
-            if (i != jt) dst[(int64_t)c * rank + r] = acc[tile][v];
+            dst[(int64_t)r * rank + c] = acc[0][tile][v];
+            if (i != jt) dst[(int64_t)c * rank + r] = acc[0][tile][v];
           }
         }
         ++tile;
