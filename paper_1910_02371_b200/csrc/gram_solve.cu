@@ -272,12 +272,6 @@ gram_kernel(const GramParams<T> p) {
 #ifndef CPFIT_GRAM_FRAG_U
 #define CPFIT_GRAM_FRAG_U 2
 #endif
-#ifndef CPFIT_GRAM_FRAG_NACC
-#define CPFIT_GRAM_FRAG_NACC 1
-#endif
-#ifndef CPFIT_GRAM_FRAG_MINB
-#define CPFIT_GRAM_FRAG_MINB 1
-#endif
 constexpr int GRAM_FRAG_WARPS = 4;
 
 template <int RT, int NPT, int U>
@@ -328,7 +322,7 @@ __device__ __forceinline__ void gram_frag_load(const GramParams<double> &p, int6
 }
 
 template <int RT, int NPT, int U>
-__global__ void __launch_bounds__(GRAM_FRAG_WARPS * 32, CPFIT_GRAM_FRAG_MINB)
+__global__ void __launch_bounds__(GRAM_FRAG_WARPS * 32)
 gram_frag_kernel(const GramParams<double> p) {
   constexpr int NT = RT * (RT + 1) / 2;
   constexpr int KS = 4 * U;  // entries per stage
@@ -339,12 +333,9 @@ gram_frag_kernel(const GramParams<double> p) {
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t t = warp; t < p.ntasks; t += nwarps) {
     const int64_t b0 = p.task_begin[t], b1 = p.task_begin[t + 1];
-    constexpr int NA = CPFIT_GRAM_FRAG_NACC;  // independent accumulator chains
-    double acc[NA][NT][2];
+    double acc[NT][2];
 #pragma unroll
-    for (int a = 0; a < NA; ++a)
-#pragma unroll
-      for (int i = 0; i < NT; ++i) acc[a][i][0] = acc[a][i][1] = 0.0;
+    for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = 0.0;
     double racc[RT];
 #pragma unroll
     for (int i = 0; i < RT; ++i) racc[i] = 0.0;
@@ -379,7 +370,7 @@ gram_frag_kernel(const GramParams<double> p) {
           for (int i = 0; i < RT; ++i)
 #pragma unroll
             for (int jt = i; jt < RT; ++jt) {
-              dmma_8x8x4(acc[u % NA][tile][0], acc[u % NA][tile][1], f[i], f[jt]);
+              dmma_8x8x4(acc[tile][0], acc[tile][1], f[i], f[jt]);
               ++tile;
             }
         }
@@ -403,13 +394,6 @@ gram_frag_kernel(const GramParams<double> p) {
           if (8 * i + gq < rank) rdst[8 * i + gq] = racc[i];
       }
     }
-#pragma unroll
-    for (int a = 1; a < NA; ++a)
-#pragma unroll
-      for (int i = 0; i < NT; ++i) {
-        acc[0][i][0] += acc[a][i][0];
-        acc[0][i][1] += acc[a][i][1];
-      }
     // accumulator fragment (tile (i, jt), element v) = G[8 i + gq][8 jt + 2 tq + v]
     int tile = 0;
 #pragma unroll
@@ -420,8 +404,8 @@ gram_frag_kernel(const GramParams<double> p) {
         for (int v = 0; v < 2; ++v) {
           const int r = 8 * i + gq, c = 8 * jt + 2 * tq + v;
           if (r < rank && c < rank) {
-            dst[(int64_t)r * rank + c] = acc[0][tile][v];
-            if (i != jt) dst[(int64_t)c * rank + r] = acc[0][tile][v];
+            dst[(int64_t)r * rank + c] = acc[tile][v];
+            if (i != jt) dst[(int64_t)c * rank + r] = acc[tile][v];
           }
         }
         ++tile;
@@ -444,6 +428,21 @@ __global__ void combine_gram_partials(const int32_t *__restrict__ split_row,
       if (c < rr) gram[row * rr + c] = (T)acc;
       else rhs[row * rank + (c - rr)] = (T)acc;
     }
+  }
+}
+
+// zero G (and rhs) of the rows without entries: warp per row
+template <typename T>
+__global__ void zero_empty_rows(int64_t dim, const int64_t *__restrict__ offsets, int64_t rr,
+                                T *__restrict__ gram, T *__restrict__ rhs, int rank) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < dim; i += nwarps) {
+    if (offsets[i + 1] != offsets[i]) continue;
+    for (int64_t c = lane; c < rr; c += 32) gram[i * rr + c] = T(0);
+    if (rhs)
+      for (int c = lane; c < rank; c += 32) rhs[i * rank + c] = T(0);
   }
 }
 
@@ -563,11 +562,18 @@ static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
       return CPFIT_ENEGWEIGHT;
     }
   }
-  CPFIT_CUDA(cudaMemsetAsync(gram, 0, (size_t)dim * rr * sizeof(T), s));
-  if (vals) CPFIT_CUDA(cudaMemsetAsync(rhs, 0, (size_t)dim * rank * sizeof(T), s));
-  if (pt->nnz == 0) return CPFIT_OK;
+  if (pt->nnz == 0) {
+    CPFIT_CUDA(cudaMemsetAsync(gram, 0, (size_t)dim * rr * sizeof(T), s));
+    if (vals) CPFIT_CUDA(cudaMemsetAsync(rhs, 0, (size_t)dim * rank * sizeof(T), s));
+    return CPFIT_OK;
+  }
   CPFIT_TRY(ensure_coarse_layout(pt, mode, s));
   CpfitModeLayout &L = pt->coarse[mode];
+  // every non-empty row is written by the Gram kernel (or its partial-slot
+  // combine); only empty rows need zeros -- no full memset of dim * R^2
+  zero_empty_rows<T><<<grid_for(dim * 32, 256), 256, 0, s>>>(dim, L.offsets, rr, gram,
+                                                             vals ? rhs : nullptr, rank);
+  CPFIT_LAUNCH_CHECK("zero_empty_rows");
   GramParams<T> p{};
   p.rank = rank;
   int np = 0;
