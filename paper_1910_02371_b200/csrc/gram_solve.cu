@@ -485,7 +485,11 @@ static bool gram_frag_enabled() {
 template <typename T, int RT, int VEC, int NPT>
 static int launch_gram_v(const GramParams<T> &p, cudaStream_t s) {
   if constexpr (sizeof(T) == 8 && (NPT == 2 || NPT == 3) && RT <= 4) {
-    if (gram_frag_enabled())
+    // weighted Grams (solve_factor, Gauss-Newton, generalized losses) keep the
+    // staged kernel: its lane groups take one sqrt(w) per entry, the fragment
+    // kernel would recompute it on the 8 lanes sharing an entry (measured:
+    // GN step 159 -> 171 ms, Poisson ALS 234 -> 257 ms with the fragment kernel)
+    if (gram_frag_enabled() && !p.weights)
       return launch_gram_frag<RT, NPT>(reinterpret_cast<const GramParams<double> &>(p), s);
   }
   constexpr int LD = gram_ld<RT>();

@@ -27,7 +27,7 @@
 #define CPFIT_TTTP_MINB 2
 #endif
 #ifndef CPFIT_MTTKRP_MINB
-#define CPFIT_MTTKRP_MINB 3
+#define CPFIT_MTTKRP_MINB 4
 #endif
 #ifndef CPFIT_MTTKRP_U
 #define CPFIT_MTTKRP_U 4  // sub-iterations of gathers in flight per MTTKRP round
