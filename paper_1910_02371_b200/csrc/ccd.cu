@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
   if (c < nchunks) ccd_load_batch<NO, U, FOLD>(p, c, 0, lane, cur);
   int32_t first_row = 0, last_row = 0, carry_row = -1;
   bool first_cont = false, last_cont = false;
-  double cnum = 0.0, cden = 0.0;
+  double la = 0.0, lb = 0.0;  // this lane's share of the carried row's (num, den)
   while (c < nchunks) {
     const int64_t c0 = c * CCD_FLAT_CHUNK;
     const int64_t c1 = min(c0 + (int64_t)CCD_FLAT_CHUNK, p.nnz);
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
       first_cont = c0 > 0 && __ldg(key + c0 - 1) == first_row;
       last_cont = c1 < p.nnz && __ldg(key + c1) == last_row;
       carry_row = -1;
-      cnum = cden = 0.0;
+      la = lb = 0.0;
     }
     // software pipeline: the next batch's stream loads are in flight while
     // this batch gathers, multiplies and scans
@@ -351,35 +351,60 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int32_t r = cur.row[u];
+      // fast path: the whole step continues the carried row -- per-lane sums
+      if (__all_sync(0xffffffffu, r == carry_row)) {
+        la += w1[u];
+        lb += w2[u];
+        continue;
+      }
+      // a boundary in this step: lanes of the carried row (a prefix) finish
+      // it, its total is the fixed butterfly over the lane sums
       double a = w1[u], b = w2[u];
+      int32_t rs = r;
+      if (r == carry_row) {
+        la += a;
+        lb += b;
+        a = b = 0.0;
+        rs = -3;  // excluded from the scan below
+      }
+      if (carry_row >= 0) {
+        double ta = la, tb = lb;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ta += __shfl_xor_sync(0xffffffffu, ta, o);
+          tb += __shfl_xor_sync(0xffffffffu, tb, o);
+        }
+        if (lane == 0)
+          ccd_emit(p, c, carry_row, ta, tb, first_row, first_cont, last_row, last_cont, pf, pl);
+      }
+      // the remaining rows of the step: segmented scan (fixed shuffle tree)
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const double ua = __shfl_up_sync(0xffffffffu, a, d);
         const double ub = __shfl_up_sync(0xffffffffu, b, d);
-        const int32_t ur = __shfl_up_sync(0xffffffffu, r, d);
-        if (lane >= d && ur == r) {
+        const int32_t ur = __shfl_up_sync(0xffffffffu, rs, d);
+        if (lane >= d && ur == rs) {
           a = ua + a;
           b = ub + b;
         }
       }
-      const int32_t next = __shfl_down_sync(0xffffffffu, r, 1);
-      const int32_t r0 = __shfl_sync(0xffffffffu, r, 0);
-      if (lane == 0 && carry_row >= 0 && r0 != carry_row)  // carried row ended last step
-        ccd_emit(p, c, carry_row, cnum, cden, first_row, first_cont, last_row, last_cont, pf, pl);
-      if (r == r0 && r == carry_row) {  // first segment continues the carry
-        a = cnum + a;
-        b = cden + b;
-      }
-      const bool tail = lane == 31 || next != r;
-      if (tail && lane < 31 && r >= 0)
-        ccd_emit(p, c, r, a, b, first_row, first_cont, last_row, last_cont, pf, pl);
-      carry_row = __shfl_sync(0xffffffffu, r, 31);  // padded lanes leave -2 (nothing carried)
-      cnum = __shfl_sync(0xffffffffu, a, 31);
-      cden = __shfl_sync(0xffffffffu, b, 31);
+      const int32_t next = __shfl_down_sync(0xffffffffu, rs, 1);
+      if (lane < 31 && next != rs && rs >= 0)
+        ccd_emit(p, c, rs, a, b, first_row, first_cont, last_row, last_cont, pf, pl);
+      // the last segment continues: its step sum seeds lane 31's accumulator
+      carry_row = __shfl_sync(0xffffffffu, rs, 31);  // padded lanes leave -2 (nothing carried)
+      la = (lane == 31 && carry_row >= 0) ? a : 0.0;
+      lb = (lane == 31 && carry_row >= 0) ? b : 0.0;
     }
-    if (nb == 0) {  // chunk done: flush the carry
-      if (lane == 0 && carry_row >= 0)
-        ccd_emit(p, c, carry_row, cnum, cden, first_row, first_cont, last_row, last_cont, pf, pl);
+    if (nb == 0 && carry_row >= 0) {  // chunk done: flush the carried row
+      double ta = la, tb = lb;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ta += __shfl_xor_sync(0xffffffffu, ta, o);
+        tb += __shfl_xor_sync(0xffffffffu, tb, o);
+      }
+      if (lane == 0)
+        ccd_emit(p, c, carry_row, ta, tb, first_row, first_cont, last_row, last_cont, pf, pl);
     }
     cur = nxt;
     c = nc;
