@@ -340,29 +340,19 @@ gram_frag_kernel(const GramParams<double> p) {
 #pragma unroll
     for (int i = 0; i < RT; ++i) racc[i] = 0.0;
     int32_t ix_next[U][NPT];
-    GramFragStage<RT, NPT, U> cur;
-    {
-      int32_t ix0[U][NPT];
-      gram_frag_idx<RT, NPT, U>(p, b0, b1, tq, ix0);
-      gram_frag_idx<RT, NPT, U>(p, b0 + KS, b1, tq, ix_next);
-      gram_frag_load<RT, NPT, U>(p, b0, b1, gq, tq, ix0, cur);
-    }
-    for (int64_t kb = b0; kb < b1; kb += KS) {
-      // next stage's gathers (indices loaded one stage earlier) and the
-      // indices of the stage after it are issued before this stage's MMAs
-      GramFragStage<RT, NPT, U> nxt;
-      gram_frag_load<RT, NPT, U>(p, kb + KS, b1, gq, tq, ix_next, nxt);
-      gram_frag_idx<RT, NPT, U>(p, kb + 2 * KS, b1, tq, ix_next);
+    // two stage buffers used alternately (no register copies between stages)
+    GramFragStage<RT, NPT, U> sa, sb;
+    auto mma_stage = [&](const GramFragStage<RT, NPT, U> &st, int64_t kb) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         double f[RT];
 #pragma unroll
         for (int i = 0; i < RT; ++i) {
-          double prod = cur.x[u][0][i];
+          double prod = st.x[u][0][i];
 #pragma unroll
-          for (int n = 1; n < NPT; ++n) prod *= cur.x[u][n][i];
-          f[i] = prod * cur.sw[u];
-          racc[i] = fma(cur.tv[u], prod, racc[i]);
+          for (int n = 1; n < NPT; ++n) prod *= st.x[u][n][i];
+          f[i] = prod * st.sw[u];
+          racc[i] = fma(st.tv[u], prod, racc[i]);
         }
         if (kb + 4 * u < b1) {
           int tile = 0;
@@ -375,7 +365,25 @@ gram_frag_kernel(const GramParams<double> p) {
             }
         }
       }
-      cur = nxt;
+    };
+    {
+      int32_t ix0[U][NPT];
+      gram_frag_idx<RT, NPT, U>(p, b0, b1, tq, ix0);
+      gram_frag_idx<RT, NPT, U>(p, b0 + KS, b1, tq, ix_next);
+      gram_frag_load<RT, NPT, U>(p, b0, b1, gq, tq, ix0, sa);
+    }
+    // the next stage's gathers (indices loaded one stage earlier) and the
+    // indices of the stage after it are issued before this stage's MMAs
+    for (int64_t kb = b0; kb < b1;) {
+      gram_frag_load<RT, NPT, U>(p, kb + KS, b1, gq, tq, ix_next, sb);
+      gram_frag_idx<RT, NPT, U>(p, kb + 2 * KS, b1, tq, ix_next);
+      mma_stage(sa, kb);
+      kb += KS;
+      if (kb >= b1) break;
+      gram_frag_load<RT, NPT, U>(p, kb + KS, b1, gq, tq, ix_next, sa);
+      gram_frag_idx<RT, NPT, U>(p, kb + 2 * KS, b1, tq, ix_next);
+      mma_stage(sb, kb);
+      kb += KS;
     }
     const int slot = p.task_slot[t];
     double *dst = slot < 0 ? p.gram + (int64_t)p.task_row[t] * rank * rank
