@@ -157,6 +157,21 @@ int cpfit_tttp_host(cpfit_pattern *p, int dtype, int rank, const void *vals,
                     const void *const *factors, void *dev_out, void *host_out,
                     int64_t chunk, void *stream);
 
+/* As cpfit_tttp_host, but `stream` is not joined to the copies: it runs on
+ * while the device->host transfers drain, and *done receives an event that
+ * completes when host_out is filled.  The caller must pass it to
+ * cpfit_event_wait (destroy = 1) exactly once, and keep dev_out / host_out
+ * alive until then. */
+int cpfit_tttp_host_async(cpfit_pattern *p, int dtype, int rank, const void *vals,
+                          const void *const *factors, void *dev_out,
+                          void *host_out, int64_t chunk, void **done, void *stream);
+int cpfit_event_wait(void *event, int destroy);
+
+/* Device -> pinned (device-mapped) host copy done by a kernel: the PCIe
+ * writes come from the SMs, so a small result is not queued behind a large
+ * transfer left running on the copy engine.  Stream-ordered on `stream`. */
+int cpfit_copy_to_host(int64_t nbytes, const void *src, void *host_dst, void *stream);
+
 /* TTTP with an affine epilogue: out[e] = alpha * m_e + beta * vals[e], with
  * m_e = sum_r prod_n factors[n][i_n(e), r].  alpha = 2, beta = -2 gives the
  * least-squares derivative tensor 2(m - t) (losses.py:41-48, model via

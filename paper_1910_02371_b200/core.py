@@ -53,6 +53,20 @@ def current_stream() -> int:
     return _torch().cuda.current_stream().cuda_stream
 
 
+def to_host_sm(t) -> np.ndarray:
+    """Small device tensor -> numpy with the copy done by a kernel writing
+    pinned host memory (cpfit_copy_to_host): it does not queue behind a large
+    device->host DMA still draining on the copy engine."""
+    torch = _torch()
+    h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    t = t.contiguous()
+    _lib.check(_lib.load().cpfit_copy_to_host(
+        t.numel() * t.element_size(), ctypes.c_void_p(t.data_ptr()),
+        ctypes.c_void_p(h.data_ptr()), ctypes.c_void_p(current_stream())), "copy_to_host")
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()
+
+
 def to_host(t, dtype=None) -> np.ndarray:
     """Device tensor -> numpy through torch's pinned host cache: the copy is a
     direct DMA at full PCIe rate, and the pinned block goes back to torch's
@@ -261,7 +275,7 @@ class SparseTensor:
     """
 
     __slots__ = ("shape", "_keys", "_values", "_shared", "_dvals", "_sorted",
-                 "_keys_fn", "_nnz", "__weakref__")
+                 "_keys_fn", "_nnz", "_pending", "__weakref__")
 
     def __init__(self, shape, keys, values, validate: bool = True):
         shape = check_shape(shape)
@@ -283,6 +297,7 @@ class SparseTensor:
         self._dvals = {}
         self._sorted = {}
         self._keys_fn = None
+        self._pending = None
 
     # -- construction of device-born tensors --------------------------------
     @classmethod
@@ -296,6 +311,7 @@ class SparseTensor:
         t._dvals = {} if dvalues is None else {dvalues.dtype: dvalues}
         t._sorted = {}
         t._keys_fn = keys_fn
+        t._pending = None
         return t
 
     @classmethod
@@ -324,6 +340,10 @@ class SparseTensor:
 
     @property
     def values(self) -> np.ndarray:
+        if self._values is None and self._pending is not None:
+            # host values still streaming back (kernels.tttp numpy path)
+            self._values = self._pending()
+            self._pending = None
         if self._values is None:
             torch = _torch()
             dv = self._dvals.get(torch.float64)

@@ -395,3 +395,47 @@ int cpfit_sgd_update(int dtype, int64_t n, const void *a, const void *grad, doub
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// SM-driven device -> pinned-host copy: the writes cross PCIe from the SMs, so
+// a small result (an MTTKRP row block) is not queued behind a large DMA that
+// an earlier call left running on the copy engine (kernels.tttp's values).
+namespace cpfit {
+__global__ void copy_to_host_kernel(int64_t n16, const uint4 *__restrict__ src,
+                                    uint4 *__restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void copy_to_host_tail(int64_t nbytes, int64_t from, const unsigned char *src,
+                                  unsigned char *dst) {
+  for (int64_t i = from + threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace cpfit
+
+extern "C" int cpfit_copy_to_host(int64_t nbytes, const void *src, void *host_dst,
+                                  void *stream) {
+  using namespace cpfit;
+  if (nbytes <= 0) return CPFIT_OK;
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, host_dst);
+  if (e != cudaSuccess || at.type != cudaMemoryTypeHost || !at.devicePointer) {
+    cudaGetLastError();
+    set_error("host buffer is not pinned, device-mapped memory");
+    return CPFIT_EINVAL;
+  }
+  void *dst = at.devicePointer;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool aligned = ((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0);
+  int64_t n16 = aligned ? nbytes / 16 : 0;
+  if (n16) {
+    copy_to_host_kernel<<<grid_for(n16, 256), 256, 0, s>>>(n16, (const uint4 *)src, (uint4 *)dst);
+    CPFIT_LAUNCH_CHECK("copy_to_host");
+  }
+  if (n16 * 16 < nbytes) {
+    copy_to_host_tail<<<1, 256, 0, s>>>(nbytes, n16 * 16, (const unsigned char *)src,
+                                        (unsigned char *)dst);
+    CPFIT_LAUNCH_CHECK("copy_to_host_tail");
+  }
+  return CPFIT_OK;
+}

@@ -53,7 +53,7 @@ static int run_tttp(cpfit_pattern *pt, int rank, const void *vals, const void *c
 template <typename T>
 static int run_tttp_host(cpfit_pattern *pt, int rank, const void *vals,
                          const void *const *factors, void *dev_out, void *host_out,
-                         int64_t chunk, cudaStream_t s) {
+                         int64_t chunk, cudaStream_t s, cudaEvent_t *done = nullptr) {
   static cudaStream_t copy_stream[64] = {};
   static cudaEvent_t evs[64][17] = {};
   int dev = 0;
@@ -77,6 +77,12 @@ static int run_tttp_host(cpfit_pattern *pt, int rank, const void *vals,
     CPFIT_CUDA(cudaStreamWaitEvent(cs, evs[dev][k], 0));
     CPFIT_CUDA(cudaMemcpyAsync((T *)host_out + b, (const T *)dev_out + b, (e - b) * sizeof(T),
                                cudaMemcpyDeviceToHost, cs));
+  }
+  if (done) {
+    // no join: `s` runs on while the copies drain; the caller waits on *done
+    CPFIT_CUDA(cudaEventCreateWithFlags(done, cudaEventDisableTiming));
+    CPFIT_CUDA(cudaEventRecord(*done, cs));
+    return CPFIT_OK;
   }
   CPFIT_CUDA(cudaEventRecord(evs[dev][16], cs));
   CPFIT_CUDA(cudaStreamWaitEvent(s, evs[dev][16], 0));
@@ -161,6 +167,38 @@ int cpfit_tttp_host(cpfit_pattern *p, int dtype, int rank, const void *vals,
     return run_tttp_host<float>(p, rank, vals, factors, dev_out, host_out, chunk, s);
   set_error("unknown dtype %d", dtype);
   return CPFIT_EINVAL;
+}
+
+int cpfit_tttp_host_async(cpfit_pattern *p, int dtype, int rank, const void *vals,
+                          const void *const *factors, void *dev_out, void *host_out,
+                          int64_t chunk, void **done, void *stream) {
+  if (!p) { set_error("null pattern"); return CPFIT_EINVAL; }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  if (!done) { set_error("null event out"); return CPFIT_EINVAL; }
+  *done = nullptr;
+  if (p->nnz > 0 && (!dev_out || !host_out)) { set_error("null output"); return CPFIT_EINVAL; }
+  if (p->nnz == 0) return CPFIT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t ev = nullptr;
+  int st;
+  if (dtype == CPFIT_F64)
+    st = run_tttp_host<double>(p, rank, vals, factors, dev_out, host_out, chunk, s, &ev);
+  else if (dtype == CPFIT_F32)
+    st = run_tttp_host<float>(p, rank, vals, factors, dev_out, host_out, chunk, s, &ev);
+  else {
+    set_error("unknown dtype %d", dtype);
+    return CPFIT_EINVAL;
+  }
+  *done = (void *)ev;
+  return st;
+}
+
+int cpfit_event_wait(void *event, int destroy) {
+  if (!event) return CPFIT_OK;
+  cudaEvent_t ev = (cudaEvent_t)event;
+  CPFIT_CUDA(cudaEventSynchronize(ev));
+  if (destroy) CPFIT_CUDA(cudaEventDestroy(ev));
+  return CPFIT_OK;
 }
 
 int cpfit_tttp_axpby(cpfit_pattern *p, int dtype, int rank, const void *vals,

@@ -24,7 +24,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .core import SparseTensor, _dtype_code, cuda_device, current_stream, to_host
+from .core import SparseTensor, _dtype_code, cuda_device, current_stream, to_host, to_host_sm
 from .exceptions import NumericalError
 from .validation import _is_torch, check_factor, check_factor_list, check_mode
 
@@ -93,11 +93,22 @@ class _FiniteCheck:
             _lib.check(L.cpfit_check_finite(_dtype_code(d.dtype), d.numel(), _vp(d),
                                             ctypes.c_void_p(base + 4 * k), _stream()),
                        "check_finite")
+        # flags head to the host right behind the checks (written by a kernel
+        # into pinned memory: a copy-engine transfer would queue behind any
+        # large device->host copy still draining), so reading them waits for
+        # the checks only
+        self.host = torch.empty(len(self.named), dtype=torch.int32, pin_memory=True)
+        _lib.check(L.cpfit_copy_to_host(4 * len(self.named), ctypes.c_void_p(base),
+                                        ctypes.c_void_p(self.host.data_ptr()), _stream()),
+                   "copy_to_host")
+        self.done = torch.cuda.Event()
+        self.done.record()
 
     def raise_if_bad(self):
         if self.flags is None:
             return
-        bad = to_host(self.flags)
+        self.done.synchronize()
+        bad = self.host.numpy()
         for k, (name, _) in enumerate(self.named):
             if bad[k]:
                 raise ValueError(f"{name} contains non-finite entries")
@@ -142,7 +153,7 @@ def mttkrp(t: SparseTensor, factors, mode: int, threads: int = 1):
         _lib.check(_lib.load().cpfit_mttkrp(
             t.device_pattern().handle, mode, _dtype_code(dtype), rank, _vp(vals), 1,
             _ptrs(dev), _vp(out), _stream()), "mttkrp")
-    res = out if on_device else to_host(out)
+    res = out if on_device else to_host_sm(out)
     fin.raise_if_bad()
     return res
 
@@ -185,15 +196,39 @@ def tttp(t: SparseTensor, factors, h_slices: int | None = None,
             _vp(out), _stream()), "tttp")
     else:
         # numpy operands: the reference returns host values -- chunked kernel
-        # with the device->host DMA of each chunk overlapping the next chunk
+        # with the device->host DMA of each chunk overlapping the next chunk,
+        # on a library copy stream the caller's stream is NOT joined to: later
+        # calls compute while the values drain, and reading `.values` waits
+        fin.raise_if_bad()
         host = torch.empty(t.nnz, dtype=dtype, pin_memory=True)
-        _lib.check(_lib.load().cpfit_tttp_host(
+        ev = ctypes.c_void_p()
+        _lib.check(_lib.load().cpfit_tttp_host_async(
             t.device_pattern().handle, _dtype_code(dtype), rank, _vp(vals), _ptrs(dev),
-            _vp(out), _vp(host), 0, _stream()), "tttp_host")
-        torch.cuda.current_stream().synchronize()
-        res._values = host.numpy()
+            _vp(out), _vp(host), 0, ctypes.byref(ev), _stream()), "tttp_host_async")
+        res._pending = _HostValues(res, ev.value, host, out)
+        return res
     fin.raise_if_bad()
     return res
+
+
+class _HostValues:
+    """Host values of an asynchronous TTTP: resolves (waits on the copy
+    event) on first read; if the tensor is dropped unread, a finalizer waits
+    for the DMA before the pinned buffer and device output are released."""
+
+    def __init__(self, owner, event, host, dev):
+        import weakref
+        self._fin = weakref.finalize(owner, _HostValues._release, event, host, dev)
+        self.host = host
+
+    @staticmethod
+    def _release(event, host, dev):
+        if event:
+            _lib.load().cpfit_event_wait(ctypes.c_void_p(event), 1)
+
+    def __call__(self):
+        self._fin()  # waits on (and destroys) the event exactly once
+        return self.host.numpy()
 
 
 def sddmm(s: SparseTensor, u, v, threads: int = 1) -> SparseTensor:
