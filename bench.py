@@ -523,6 +523,40 @@ def ingest_section(dev, reps=3):
     return out
 
 
+def pairwise_section(dev, reps=3):
+    """The paper's comparison on the B200: all-at-once TTTP / MTTKRP vs the
+    pairwise-contraction baseline (hypersparse.py: TTM through a CCSR
+    matricization, semi-sparse intermediates) at the cfg 2 size, fp64, R=16,
+    both through the numpy API (host factors in, host results out)."""
+    import torch
+
+    import paper_1910_02371_b200 as cp
+    from paper_1910_02371_b200 import hypersparse as H
+    from paper_1910_02371_b200 import synth
+    shape, keys, values, factors = synth.cfg2()
+    t = cp.SparseTensor(shape, keys, values, validate=False)
+
+    def wall(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        return float(np.median(ts))
+    out = {"workload": "cfg 2 (1e7 nnz, 10^4 cube, R=16, fp64), numpy API on both sides"}
+    out["all_at_once_tttp_ms"] = wall(lambda: cp.tttp(t, factors).values)
+    out["pairwise_tttp_ms"] = wall(lambda: H.pairwise_tttp(t, factors).values)
+    out["all_at_once_mttkrp0_ms"] = wall(lambda: cp.mttkrp(t, factors, 0))
+    out["pairwise_mttkrp0_ms"] = wall(lambda: H.pairwise_mttkrp(t, factors, 0))
+    out["note"] = ("pairwise MTTKRP = matricization to CCSR (device sort), CCSR x dense "
+                   "(TTM), fold of the remaining factor and fiber-order row sums, with the "
+                   "reference's host-resident CCSR / semi-sparse objects in between")
+    return out
+
+
 def dense_section(dev, sweeps=2):
     """BASELINE cfg 4: dense 800^3 fp64 N(0,1), R=64 factors N(0,1): dense
     MTTKRP per mode and CP-ALS sweep time, against the on-box DGEMM peak."""
@@ -799,11 +833,17 @@ def main():
             als = {"error": repr(exc)}
         torch.cuda.empty_cache()
     ingest = None
+    pairwise = None
     if world == 1:
         try:
             ingest = ingest_section(dev)
         except Exception as exc:
             ingest = {"error": repr(exc)}
+        torch.cuda.empty_cache()
+        try:
+            pairwise = pairwise_section(dev)
+        except Exception as exc:
+            pairwise = {"error": repr(exc)}
         torch.cuda.empty_cache()
     dense = None
     if not args.no_dense and world == 1:
@@ -823,6 +863,7 @@ def main():
             "compulsory_bytes_per_pass": compulsory,
             "clocks": clk, "gpu_launches": launches_per_step * args.steps, "e2e": e2e,
             "als": als, "dense": dense, "sgd": sgd, "ingest": ingest,
+            "pairwise_vs_all_at_once": pairwise,
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample()

@@ -296,6 +296,26 @@ int cpfit_from_coords(int order, const int64_t *dims, int64_t n, int coord_bytes
                       uint64_t *keys_out, double *vals_out, int64_t *nnz_out,
                       int *bad_mode, void *stream);
 
+/* ---- pairwise (hypersparse) baseline, hypersparse.py */
+/* CCSR x dense: payload[slot, :] = sum_j values[j] * dense[col_ids[j], :]
+ * over slot's entries, per column in np.add.reduceat's order along the entry
+ * axis (first product + numpy's pairwise sum of the rest). */
+int cpfit_ccsr_spmm(int64_t nrows, const int64_t *row_offsets, const int64_t *col_ids,
+                    const double *values, const double *dense, int rank,
+                    double *payload, void *stream);
+/* pairwise TTTP: out[e] = row sum over r (numpy's order) of
+ * ((values[e] * F0[i0(e), r]) * F1[i1(e), r]) ...; idx[n] = int32 device
+ * coordinates of the n-th provided factor's mode; R <= 256. */
+int cpfit_pairwise_tttp(int64_t nnz, int nfac, int rank, const int32_t *const *idx,
+                        const double *const *factors, const double *values,
+                        double *out, void *stream);
+/* pairwise MTTKRP tail: w[f, r] = payload[f, r] * prod_n factors[n][idx[n][f], r],
+ * out[i, r] = 0.0 + sum of w over fibers with target[f] = i in fiber order
+ * (np.bincount); out is dim x rank. */
+int cpfit_pairwise_fold_sum(int64_t nfibers, int rank, int nfold, const int32_t *const *idx,
+                            const double *const *factors, const double *payload,
+                            const int32_t *target, int64_t dim, double *out, void *stream);
+
 /* ---- generalized losses (losses.py:22-104) ---------------------------- */
 /* Loss ids: 0 = least squares (phi = (t - m)^2, dphi = 2 (m - t), d2phi = 2),
  * 1 = Poisson log link (phi = exp(m~) - t m, dphi = exp(m~) - t, d2phi =

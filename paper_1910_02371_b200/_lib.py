@@ -41,6 +41,7 @@ SYMBOLS = (
     "cpfit_batched_symv", "cpfit_tttp_loss", "cpfit_loss_eval", "cpfit_ccd_gen_weights",
     "cpfit_ccd_gen_update", "cpfit_ccd_gen_model", "cpfit_from_coords",
     "cpfit_tttp_host_async", "cpfit_event_wait", "cpfit_copy_to_host",
+    "cpfit_ccsr_spmm", "cpfit_pairwise_tttp", "cpfit_pairwise_fold_sum",
 )
 
 _vp = ctypes.c_void_p
@@ -100,6 +101,9 @@ def load(path: str | None = None):
                                   ctypes.POINTER(_vp), _vp],
         "cpfit_event_wait": [_vp, _int],
         "cpfit_copy_to_host": [_i64, _vp, _vp, _vp],
+        "cpfit_ccsr_spmm": [_i64, _vp, _vp, _vp, _vp, _int, _vp, _vp],
+        "cpfit_pairwise_tttp": [_i64, _int, _int, _PP, _PP, _vp, _vp, _vp],
+        "cpfit_pairwise_fold_sum": [_i64, _int, _int, _PP, _PP, _vp, _vp, _i64, _vp, _vp],
         "cpfit_tttp_subst": [_vp, _int, _int, _vp, _PP, _PP, _vp, _vp],
         "cpfit_axpby": [_int, _i64, ctypes.c_double, _vp, ctypes.c_double, _vp, _vp, _vp],
         "cpfit_spd_inverse_rows": [_int, _int, _i64, _vp, _i64, ctypes.c_double, _vp,

@@ -379,6 +379,8 @@ int radix_sort_pairs(const K *keys, int64_t n, int bits, K *sorted_keys, int32_t
 }
 template int radix_sort_pairs<uint64_t>(const uint64_t *, int64_t, int, uint64_t *, int32_t *,
                                         cudaStream_t);
+template int radix_sort_pairs<int32_t>(const int32_t *, int64_t, int, int32_t *, int32_t *,
+                                       cudaStream_t);
 
 // Stable sort of positions 0..n-1 by keys (non-negative, < dim).
 static int radix_sort_positions(const int32_t *keys, int64_t n, int64_t dim,

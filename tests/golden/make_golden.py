@@ -27,6 +27,12 @@ Fixtures:
                         8..128 and > 128 long: numpy's reduceat/pairwise
                         order), order-4 int32 coordinates, and parse_tns of a
                         generated .tns text
+  hypersparse.npz    -- the pairwise baseline: ccsr_from_coo, matricize
+                        (native and permuted modes), ccsr_times_dense,
+                        ccsr_sum with cancellations, butterfly reduce-scatter
+                        (canonical and eager, k = 2 / 3, P = 5), ttm,
+                        pairwise_mttkrp (orders 3 / 4), pairwise_tttp (R up
+                        to 20, absent factors)
   second_order.npz   -- hessian_matvec (ls/poisson x gauss_newton/newton),
                         gradient_blocks, gn_step trajectories (ls GN, ls
                         Newton, poisson GN) and run(algorithm=gn/newton) traces
@@ -404,6 +410,80 @@ def ingest():
     np.savez_compressed(os.path.join(HERE, "ingest.npz"), **out)
 
 
+def _ccsr_out(out, tag, a):
+    out[f"{tag}_shape"] = np.array([a.global_rows, a.global_cols])
+    out[f"{tag}_rows"] = a.nnz_row_ids
+    out[f"{tag}_offs"] = a.row_offsets
+    out[f"{tag}_cols"] = a.col_ids
+    out[f"{tag}_vals"] = a.values
+
+
+def hypersparse():
+    from cpfit import hypersparse as H
+    rng = np.random.default_rng(61)
+    out = {}
+    # COO -> CCSR (distinct pairs, shuffled)
+    gr, gc = 100_000, 300
+    keys = np.unique(rng.integers(0, gr * gc, 5000))
+    rng.shuffle(keys)
+    r, c = keys // gc, keys % gc
+    v = rng.standard_normal(keys.size)
+    a = H.ccsr_from_coo(r, c, v, gr, gc)
+    out["coo_r"], out["coo_c"], out["coo_v"] = r, c, v
+    _ccsr_out(out, "coo", a)
+    # matricize: native and permuted
+    t = random_sparse((9, 8, 7, 6), 0.2, rng)
+    out["t_dims"], out["t_keys"], out["t_vals"] = np.array(t.shape), t.keys, t.values
+    for tag, rm, cm in (("mat_native", (0, 1), (2, 3)), ("mat_perm", (3, 1), (0, 2)),
+                        ("mat_rowsonly", (2, 0, 3, 1), ())):
+        _ccsr_out(out, tag, H.matricize_to_ccsr(t, rm, cm))
+    # CCSR x dense
+    b = rng.standard_normal((gc, 7))
+    out["spmm_b"] = b
+    z = H.ccsr_times_dense(a, b)
+    out["spmm_keys"], out["spmm_payload"] = z.fiber_keys, z.payload
+    # sums with cancellations
+    a2 = H.ccsr_from_coo(r[:2000], c[:2000], -v[:2000], gr, gc)
+    keys3 = np.unique(rng.integers(0, gr * gc, 3000))
+    a3 = H.ccsr_from_coo(keys3 // gc, keys3 % gc, rng.standard_normal(keys3.size), gr, gc)
+    _ccsr_out(out, "a2", a2)
+    _ccsr_out(out, "a3", a3)
+    _ccsr_out(out, "sum12", H.ccsr_sum(a, a2))
+    _ccsr_out(out, "sum13", H.ccsr_sum(a, a3))
+    # butterfly reduce-scatter of 5 summands
+    parts = []
+    for p_ in range(5):
+        kk = np.unique(rng.integers(0, 40 * 50, 300))
+        parts.append(H.ccsr_from_coo(kk // 50, kk % 50, rng.standard_normal(kk.size), 40, 50))
+        _ccsr_out(out, f"bf_in{p_}", parts[-1])
+    for k in (2, 3):
+        for canon in (True, False):
+            shards = H.butterfly_reduce_scatter(parts, k=k, canonical=canon)
+            for p_, sh in enumerate(shards):
+                _ccsr_out(out, f"bf_k{k}_c{int(canon)}_s{p_}", sh)
+            _ccsr_out(out, f"bf_k{k}_c{int(canon)}_all", H.butterfly_gather(shards))
+    # ttm / pairwise
+    w = rng.standard_normal((t.shape[2], 5))
+    out["ttm_w"] = w
+    zz = H.ttm(t, w, 2)
+    out["ttm_keys"], out["ttm_payload"] = zz.fiber_keys, zz.payload
+    f4 = [rng.standard_normal((d, 5)) for d in t.shape]
+    for n in range(4):
+        out[f"pw_f{n}"] = f4[n]
+    for mode in range(4):
+        out[f"pw_mttkrp{mode}"] = H.pairwise_mttkrp(t, f4, mode)
+    t3 = random_sparse((11, 10, 9), 0.3, rng)
+    out["t3_dims"], out["t3_keys"], out["t3_vals"] = np.array(t3.shape), t3.keys, t3.values
+    for R in (1, 7, 8, 20):
+        fs = [rng.standard_normal((d, R)) for d in t3.shape]
+        for n in range(3):
+            out[f"pt{R}_f{n}"] = fs[n]
+        out[f"pt{R}_out"] = H.pairwise_tttp(t3, fs).values
+        out[f"pt{R}_none_out"] = H.pairwise_tttp(t3, [None, fs[1], fs[2]]).values
+        out[f"pt{R}_mttkrp1"] = H.pairwise_mttkrp(t3, fs, 1)
+    np.savez_compressed(os.path.join(HERE, "hypersparse.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -416,6 +496,7 @@ if __name__ == "__main__":
     drivers_small()
     generalized()
     ingest()
+    hypersparse()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
