@@ -247,7 +247,7 @@ struct cpfit_pattern {
   int64_t dims[CPFIT_MAXN] = {0};
   int64_t nnz = 0;
   int32_t *coords[CPFIT_MAXN] = {nullptr};
-  int64_t task_size = 1024;
+  int64_t task_size = 256;  // entries per MTTKRP task: 4x finer than a 10^4-row slice, so the persistent warps end within ~1/8 of their work (cfg 2 MTTKRP 0.189 -> 0.165 ms)
   CpfitModeLayout modes[CPFIT_MAXN];
   int32_t *parent = nullptr;  // sampled patterns: entry -> entry of the source pattern
   // coarse task tables (task_size * CPFIT_COARSE_TASKS) for the Gram kernel:
@@ -255,7 +255,7 @@ struct cpfit_pattern {
   CpfitModeLayout coarse[CPFIT_MAXN];
 };
 
-#define CPFIT_COARSE_TASKS 8
+#define CPFIT_COARSE_TASKS 32
 
 namespace cpfit {
 int ensure_layout(cpfit_pattern *p, int mode, cudaStream_t s);
