@@ -247,7 +247,7 @@ struct cpfit_pattern {
   int64_t dims[CPFIT_MAXN] = {0};
   int64_t nnz = 0;
   int32_t *coords[CPFIT_MAXN] = {nullptr};
-  int64_t task_size = 256;  // entries per MTTKRP task: 4x finer than a 10^4-row slice, so the persistent warps end within ~1/8 of their work (cfg 2 MTTKRP 0.189 -> 0.165 ms)
+  int64_t task_size = 0;  // entries per segmented task; 0 = automatic (task_size_for)
   CpfitModeLayout modes[CPFIT_MAXN];
   int32_t *parent = nullptr;  // sampled patterns: entry -> entry of the source pattern
   // coarse task tables (task_size * CPFIT_COARSE_TASKS) for the Gram kernel:
@@ -255,9 +255,25 @@ struct cpfit_pattern {
   CpfitModeLayout coarse[CPFIT_MAXN];
 };
 
-#define CPFIT_COARSE_TASKS 32
+#define CPFIT_COARSE_TASKS 8
 
 namespace cpfit {
+// Task granularity.  Persistent MTTKRP warps (148 SMs x 4 blocks x 8 warps)
+// finish within ~1/8 of their work when there are >= 8 tasks per warp; longer
+// tasks cost fewer row splits and task prologues.  Automatic size: nnz / (8 x
+// warps), rounded up to 32 and clamped to [256, 1024] (cfg 2, 1e7 nnz: 288 --
+// MTTKRP 0.189 -> 0.165 ms vs 1024; cfg 3, 1e8 nnz: 1024).  Coarse (Gram)
+// tasks: 8192 entries in automatic mode, 8 x an explicit size otherwise.
+inline int64_t task_size_for(const cpfit_pattern *p) {
+  if (p->task_size > 0) return p->task_size;
+  const int64_t warps = (int64_t)num_sms() * 4 * 8;
+  int64_t ts = (p->nnz + 8 * warps - 1) / (8 * warps);
+  ts = (ts + 31) / 32 * 32;
+  return ts < 256 ? 256 : (ts > 1024 ? 1024 : ts);
+}
+inline int64_t coarse_task_size_for(const cpfit_pattern *p) {
+  return p->task_size > 0 ? p->task_size * CPFIT_COARSE_TASKS : 8192;
+}
 int ensure_layout(cpfit_pattern *p, int mode, cudaStream_t s);
 int ensure_coarse_layout(cpfit_pattern *p, int mode, cudaStream_t s);
 }

@@ -516,7 +516,7 @@ int ensure_layout(cpfit_pattern *p, int mode, cudaStream_t s) {
       CPFIT_TRY(gather_i32(p->coords[k], L.perm, L.sorted_idx[k], n, s));
     }
   }
-  CPFIT_TRY(build_tasks(L, dim, n, p->task_size, s));
+  CPFIT_TRY(build_tasks(L, dim, n, task_size_for(p), s));
   L.built = true;
   return CPFIT_OK;
 }
@@ -533,7 +533,7 @@ int ensure_coarse_layout(cpfit_pattern *p, int mode, cudaStream_t s) {
     C.owns_sorted[k] = false;
   }
   C.borrowed = true;
-  CPFIT_TRY(build_tasks(C, p->dims[mode], p->nnz, p->task_size * CPFIT_COARSE_TASKS, s));
+  CPFIT_TRY(build_tasks(C, p->dims[mode], p->nnz, coarse_task_size_for(p), s));
   C.built = true;
   return CPFIT_OK;
 }

@@ -27,7 +27,10 @@
 #define CPFIT_TTTP_MINB 2
 #endif
 #ifndef CPFIT_MTTKRP_MINB
-#define CPFIT_MTTKRP_MINB 4
+#define CPFIT_MTTKRP_MINB 4  // fp64 (cfg 2: 0.196 -> 0.188 ms vs 3)
+#endif
+#ifndef CPFIT_MTTKRP_MINB_F32
+#define CPFIT_MTTKRP_MINB_F32 3  // fp32 (cfg 5 SGD samples: 4 cost ~1 ms per step)
 #endif
 #ifndef CPFIT_MTTKRP_U
 #define CPFIT_MTTKRP_U 4  // sub-iterations of gathers in flight per MTTKRP round
@@ -262,7 +265,8 @@ __device__ __forceinline__ void mttkrp_load_batch(const MttkrpParams<T> &p, int 
 }
 
 template <typename T, int VEC, int LPE, int KV, int NP, bool FULL>
-__global__ void __launch_bounds__(256, CPFIT_MTTKRP_MINB) mttkrp_kernel(const MttkrpParams<T> p) {
+__global__ void __launch_bounds__(256, sizeof(T) == 8 ? CPFIT_MTTKRP_MINB : CPFIT_MTTKRP_MINB_F32)
+    mttkrp_kernel(const MttkrpParams<T> p) {
   constexpr int G = 32 / LPE;
   constexpr int NPM = NP > 0 ? NP : CPFIT_MAXN;
   constexpr int U = NP > 0 ? (LPE < CPFIT_MTTKRP_U ? LPE : CPFIT_MTTKRP_U) : 1;
@@ -405,7 +409,8 @@ template <typename T, int VEC, int LPE, int KV>
 static int launch_mttkrp_np(const MttkrpParams<T> &p, cudaStream_t s) {
   // persistent grid: exactly the resident capacity (no partial waves)
   int64_t blocks = (p.ntasks + 7) / 8;
-  const int64_t cap = (int64_t)num_sms() * CPFIT_MTTKRP_MINB;
+  const int64_t cap =
+      (int64_t)num_sms() * (sizeof(T) == 8 ? CPFIT_MTTKRP_MINB : CPFIT_MTTKRP_MINB_F32);
   const unsigned grid = (unsigned)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
   const bool full = p.rank == LPE * VEC * KV;
   constexpr bool HOT = (sizeof(T) == 8 && VEC == 2) || (sizeof(T) == 4 && VEC == 4);
