@@ -612,6 +612,8 @@ def main():
     ap.add_argument("--no-als", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-sgd", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the ingest and pairwise-vs-all-at-once sections")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -834,7 +836,7 @@ def main():
         torch.cuda.empty_cache()
     ingest = None
     pairwise = None
-    if world == 1:
+    if world == 1 and not args.no_extra:
         try:
             ingest = ingest_section(dev)
         except Exception as exc:
