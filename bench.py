@@ -301,6 +301,9 @@ def als_section(world, rank, dev, sweeps=3):
         from paper_1910_02371_b200.losses import ls_data_term
         out["rmse_after"] = float(np.sqrt(ls_data_term(t, F) / t.nnz))
         F = [f.clone() for f in init]
+        _ccd_ls_device(t, F, REG)  # warm-up: the per-mode rhat copies' allocations
+        F = [f.clone() for f in init]
+        torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         _ccd_ls_device(t, F, REG)

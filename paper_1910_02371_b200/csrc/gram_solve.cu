@@ -55,6 +55,7 @@ struct GramParams {
   const T *vals;          // nullable: no rhs
   const int32_t *vperm;   // non-null: vals in canonical order, gather by perm
   T *rhs;                 // dims[mode] x R
+  const double *sqrt_w;   // fragment kernel: sqrt(weights) in sorted order (nullable)
 };
 
 constexpr int GRAM_WARPS = 4;
@@ -313,7 +314,8 @@ __device__ __forceinline__ void gram_frag_load(const GramParams<double> &p, int6
     double sw = 0.0, tv = 0.0;
     if (ok) {
       sw = 1.0;
-      if (p.weights) sw = sqrt(p.wperm ? __ldg(p.weights + __ldg(p.wperm + e)) : __ldg(p.weights + e));
+      if (p.sqrt_w) sw = __ldg(p.sqrt_w + e);  // sqrt(w) precomputed in sorted order
+      else if (p.weights) sw = sqrt(p.wperm ? __ldg(p.weights + __ldg(p.wperm + e)) : __ldg(p.weights + e));
       if (p.vals) tv = p.vperm ? __ldg(p.vals + __ldg(p.vperm + e)) : __ldg(p.vals + e);
     }
     st.sw[u] = sw;
@@ -454,6 +456,17 @@ __global__ void zero_empty_rows(int64_t dim, const int64_t *__restrict__ offsets
   }
 }
 
+// sqrt(w) of every entry in mode-sorted order (the fragment Gram kernel's
+// per-entry scale; computed once instead of on the 8 lanes sharing an entry)
+template <typename T>
+__global__ void sqrt_weights_kernel(int64_t n, const T *__restrict__ w,
+                                    const int32_t *__restrict__ wperm,
+                                    double *__restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = sqrt((double)(wperm ? w[wperm[e]] : w[e]));
+}
+
 template <typename T>
 __global__ void check_weights_kernel(const T *__restrict__ w, int64_t n, int *flag) {
   int bad = 0;
@@ -493,11 +506,10 @@ static bool gram_frag_enabled() {
 template <typename T, int RT, int VEC, int NPT>
 static int launch_gram_v(const GramParams<T> &p, cudaStream_t s) {
   if constexpr (sizeof(T) == 8 && (NPT == 2 || NPT == 3) && RT <= 4) {
-    // weighted Grams (solve_factor, Gauss-Newton, generalized losses) keep the
-    // staged kernel: its lane groups take one sqrt(w) per entry, the fragment
-    // kernel would recompute it on the 8 lanes sharing an entry (measured:
-    // GN step 159 -> 171 ms, Poisson ALS 234 -> 257 ms with the fragment kernel)
-    if (gram_frag_enabled() && !p.weights)
+    // weighted Grams (solve_factor, Gauss-Newton, generalized losses) reach
+    // the fragment kernel with sqrt(w) precomputed per entry (run_gram): it
+    // would otherwise recompute it on the 8 lanes sharing an entry
+    if (gram_frag_enabled() && (!p.weights || p.sqrt_w))
       return launch_gram_frag<RT, NPT>(reinterpret_cast<const GramParams<double> &>(p), s);
   }
   constexpr int LD = gram_ld<RT>();
@@ -618,6 +630,15 @@ static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
   Scratch<T> partial(s);
   if (L.nslots > 0) CPFIT_TRY(partial.alloc((size_t)L.nslots * p.pstride));
   p.partial = partial.ptr;
+  Scratch<double> sqw(s);
+  if (sizeof(T) == 8 && weights && np == 2 && rank <= 32 &&
+      gram_frag_enabled()) {
+    CPFIT_TRY(sqw.alloc(pt->nnz));
+    sqrt_weights_kernel<T><<<grid_for(pt->nnz, 256, 4), 256, 0, s>>>(
+        pt->nnz, weights, p.wperm, sqw.ptr);
+    CPFIT_LAUNCH_CHECK("sqrt_weights");
+    p.sqrt_w = sqw.ptr;
+  }
   CPFIT_TRY(launch_gram<T>(p, s));
   if (L.nsplit > 0) {
     unsigned grid = (unsigned)(L.nsplit < 65535 ? L.nsplit : 65535);
