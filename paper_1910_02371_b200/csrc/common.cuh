@@ -233,6 +233,7 @@ struct CpfitModeLayout {
   bool owns_sorted[CPFIT_MAXN] = {false};
   // segmented-work tasks
   int64_t ntasks = 0, nslots = 0, nsplit = 0, task_size = 0;
+  int64_t max_slots = 0;          // most tasks of one slice
   int64_t *task_begin = nullptr;  // ntasks + 1
   int32_t *task_row = nullptr;    // ntasks
   int32_t *task_slot = nullptr;   // ntasks (-1 = row owned by one task)

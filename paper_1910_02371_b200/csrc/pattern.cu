@@ -397,7 +397,8 @@ static int radix_sort_positions(const int32_t *keys, int64_t n, int64_t dim,
 
 __global__ void task_count_kernel(const int64_t *__restrict__ offsets, int64_t dim, int64_t L,
                                   int32_t *__restrict__ nt, int32_t *__restrict__ nslot,
-                                  int32_t *__restrict__ split) {
+                                  int32_t *__restrict__ split, int *__restrict__ max_t) {
+  int mt = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < dim;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t len = offsets[i + 1] - offsets[i];
@@ -405,7 +406,9 @@ __global__ void task_count_kernel(const int64_t *__restrict__ offsets, int64_t d
     nt[i] = (int32_t)t;
     nslot[i] = t > 1 ? (int32_t)t : 0;
     split[i] = t > 1 ? 1 : 0;
+    mt = t > mt ? (int)t : mt;
   }
+  if (mt) atomicMax(max_t, mt);
 }
 
 __global__ void task_fill_kernel(const int64_t *__restrict__ offsets, int64_t dim,
@@ -443,6 +446,9 @@ static int build_tasks(CpfitModeLayout &L, int64_t dim, int64_t nnz, int64_t tas
                        cudaStream_t s) {
   Scratch<int32_t> nt(s), nslot(s), split(s);
   Scratch<int64_t> tstart(s), sstart(s), xstart(s);
+  Scratch<int> maxt(s);
+  CPFIT_TRY(maxt.alloc(1));
+  CPFIT_CUDA(cudaMemsetAsync(maxt.ptr, 0, sizeof(int), s));
   CPFIT_TRY(nt.alloc(dim));
   CPFIT_TRY(nslot.alloc(dim));
   CPFIT_TRY(split.alloc(dim));
@@ -450,7 +456,7 @@ static int build_tasks(CpfitModeLayout &L, int64_t dim, int64_t nnz, int64_t tas
   CPFIT_TRY(sstart.alloc(dim + 1));
   CPFIT_TRY(xstart.alloc(dim + 1));
   task_count_kernel<<<grid_for(dim, 256), 256, 0, s>>>(L.offsets, dim, task_size, nt.ptr,
-                                                       nslot.ptr, split.ptr);
+                                                       nslot.ptr, split.ptr, maxt.ptr);
   CPFIT_LAUNCH_CHECK("task_count");
   CPFIT_TRY(exclusive_scan<int32_t>(nt.ptr, tstart.ptr, dim, s));
   CPFIT_TRY(exclusive_scan<int32_t>(nslot.ptr, sstart.ptr, dim, s));
@@ -459,7 +465,10 @@ static int build_tasks(CpfitModeLayout &L, int64_t dim, int64_t nnz, int64_t tas
   CPFIT_CUDA(cudaMemcpyAsync(&tot[0], tstart.ptr + dim, 8, cudaMemcpyDeviceToHost, s));
   CPFIT_CUDA(cudaMemcpyAsync(&tot[1], sstart.ptr + dim, 8, cudaMemcpyDeviceToHost, s));
   CPFIT_CUDA(cudaMemcpyAsync(&tot[2], xstart.ptr + dim, 8, cudaMemcpyDeviceToHost, s));
+  int hmax = 0;
+  CPFIT_CUDA(cudaMemcpyAsync(&hmax, maxt.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
   CPFIT_CUDA(cudaStreamSynchronize(s));
+  L.max_slots = hmax;
   L.ntasks = tot[0];
   L.nslots = tot[1];
   L.nsplit = tot[2];

@@ -133,6 +133,12 @@ static int run_mttkrp(cpfit_pattern *pt, int mode, int rank, const void *vals, i
     combine_partials<T><<<grid_for(L.nsplit * 32, 256), 256, 0, s>>>(
         L.split_row, L.split_slot, L.nsplit, rank, partial.ptr, (T *)out);
     CPFIT_LAUNCH_CHECK("combine_partials");
+    if (L.max_slots > COMBINE_LONG) {  // block per long row; the others exit
+      const int64_t lb = L.nsplit < (int64_t)num_sms() * 8 ? L.nsplit : (int64_t)num_sms() * 8;
+      combine_partials_long<T><<<(unsigned)(lb > 0 ? lb : 1), 256, 0, s>>>(
+          L.split_row, L.split_slot, L.nsplit, rank, partial.ptr, (T *)out);
+      CPFIT_LAUNCH_CHECK("combine_partials_long");
+    }
   }
   return CPFIT_OK;
 }

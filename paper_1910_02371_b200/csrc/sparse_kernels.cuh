@@ -356,7 +356,13 @@ __global__ void __launch_bounds__(256, sizeof(T) == 8 ? CPFIT_MTTKRP_MINB : CPFI
   }
 }
 
-// Sum the partial rows of split slices in task order.
+// Sum the partial rows of split slices in a fixed order (deterministic).
+// Rows with few slots: warp per row, slots summed in task order (lane =
+// column).  Rows with many slots (Zipf heads: thousands): block per row,
+// warp w takes slots a + w, a + w + 8, ..., then the 8 warp sums are added in
+// warp order.  Each kernel skips the other's rows.
+constexpr int COMBINE_LONG = 64;
+
 template <typename T>
 __global__ void combine_partials(const int32_t *__restrict__ split_row,
                                  const int32_t *__restrict__ split_slot, int64_t nsplit,
@@ -365,12 +371,41 @@ __global__ void combine_partials(const int32_t *__restrict__ split_row,
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = warp; s < nsplit; s += nwarps) {
-    const int64_t row = split_row[s];
     const int64_t a = split_slot[s], b = split_slot[s + 1];
+    if (b - a > COMBINE_LONG) continue;
+    const int64_t row = split_row[s];
     for (int c = lane; c < rank; c += 32) {
       T acc = partial[a * rank + c];
       for (int64_t k = a + 1; k < b; ++k) acc += partial[k * rank + c];
       out[row * rank + c] = acc;
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) combine_partials_long(
+    const int32_t *__restrict__ split_row, const int32_t *__restrict__ split_slot,
+    int64_t nsplit, int rank, const T *__restrict__ partial, T *__restrict__ out) {
+  __shared__ T red[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t s = blockIdx.x; s < nsplit; s += gridDim.x) {
+    const int64_t a = split_slot[s], b = split_slot[s + 1];
+    if (b - a <= COMBINE_LONG) continue;  // block-uniform
+    const int64_t row = split_row[s];
+    for (int c0 = 0; c0 < rank; c0 += 32) {
+      const int c = c0 + lane;
+      T acc = T(0);
+      if (c < rank)
+        for (int64_t k = a + w; k < b; k += 8) acc += partial[k * rank + c];
+      red[w][lane] = acc;
+      __syncthreads();
+      if (w == 0 && c < rank) {
+        T tot = red[0][lane];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) tot += red[j][lane];
+        out[row * rank + c] = tot;
+      }
+      __syncthreads();
     }
   }
 }
