@@ -33,6 +33,8 @@ Fixtures:
                         (canonical and eager, k = 2 / 3, P = 5), ttm,
                         pairwise_mttkrp (orders 3 / 4), pairwise_tttp (R up
                         to 20, absent factors)
+  cli.npz            -- `cpfit gen` output bytes and `cpfit run --deterministic`
+                        trace CSVs (als / ccd / sgd / gn, ls and poisson)
   second_order.npz   -- hessian_matvec (ls/poisson x gauss_newton/newton),
                         gradient_blocks, gn_step trajectories (ls GN, ls
                         Newton, poisson GN) and run(algorithm=gn/newton) traces
@@ -484,6 +486,37 @@ def hypersparse():
     np.savez_compressed(os.path.join(HERE, "hypersparse.npz"), **out)
 
 
+def cli():
+    import subprocess
+    import tempfile
+    env = dict(os.environ, PYTHONPATH="/root/reference/pkg/src")
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        data = os.path.join(d, "x.tns")
+        subprocess.run([sys.executable, "-m", "cpfit", "gen", "lowrank", "--dims", "12,12,12",
+                        "--rank", "3", "--fraction", "0.3", "--seed", "5", "--out", data],
+                       check=True, env=env, capture_output=True)
+        out["gen_tns"] = np.array(open(data).read())
+        out["gen_factors"] = np.frombuffer(open(data + ".factors.npy", "rb").read(), np.uint8)
+        pdata = os.path.join(d, "p.tns")
+        subprocess.run([sys.executable, "-m", "cpfit", "gen", "function", "--dims", "8,7,6",
+                        "--fraction", "0.5", "--seed", "2", "--out", pdata],
+                       check=True, env=env, capture_output=True)
+        out["gen_function_tns"] = np.array(open(pdata).read())
+        runs = {"als": ["--algo", "als"], "ccd": ["--algo", "ccd"],
+                "sgd": ["--algo", "sgd", "--sample-rate", "0.5", "--step", "0.01"],
+                "gn": ["--algo", "gn"],
+                "als_poisson": ["--algo", "als", "--loss", "poisson"]}
+        for tag, extra in runs.items():
+            tr = os.path.join(d, f"{tag}.csv")
+            src = pdata if tag.endswith("poisson") else data
+            subprocess.run([sys.executable, "-m", "cpfit", "run", "--input", src, "--rank", "3",
+                            "--max-iters", "5", "--seed", "11", "--deterministic",
+                            "--trace", tr, *extra], check=True, env=env, capture_output=True)
+            out[f"trace_{tag}"] = np.array(open(tr).read())
+    np.savez_compressed(os.path.join(HERE, "cli.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -497,6 +530,7 @@ if __name__ == "__main__":
     generalized()
     ingest()
     hypersparse()
+    cli()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
