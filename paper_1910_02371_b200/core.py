@@ -41,16 +41,35 @@ def _torch():
     return torch
 
 
+_DEVICES: dict = {}
+_CUDA_OK = None
+
+
 def cuda_device():
+    """torch.device of the current CUDA device (cached per index: the API
+    entry points call this many times per call)."""
+    global _CUDA_OK
     torch = _torch()
-    if not torch.cuda.is_available():
+    if _CUDA_OK is None:
+        _CUDA_OK = torch.cuda.is_available()
+    if not _CUDA_OK:
         raise RuntimeError("cpfit-b200 kernels need a CUDA device (B200, sm_100a); "
                            "there is no CPU fallback")
-    return torch.device("cuda", torch.cuda.current_device())
+    idx = torch._C._cuda_getDevice()
+    dev = _DEVICES.get(idx)
+    if dev is None:
+        dev = _DEVICES[idx] = torch.device("cuda", idx)
+    return dev
 
 
 def current_stream() -> int:
-    return _torch().cuda.current_stream().cuda_stream
+    """Raw cudaStream_t of torch's current stream on the current device (the
+    library launches on it)."""
+    torch = _torch()
+    try:
+        return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
+    except AttributeError:  # older torch
+        return torch.cuda.current_stream().cuda_stream
 
 
 def to_host_sm(t) -> np.ndarray:
