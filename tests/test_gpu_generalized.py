@@ -110,3 +110,20 @@ def test_poisson_run_traces(algo):
     assert rel(met, z[f"run_{algo}_metric"]) < 1e-10
     for n in range(3):
         assert rel(state.factors[n], z[f"run_{algo}_f{n}"]) < 1e-9
+
+
+def test_poisson_sgd_fp32_device_factors_close_to_fp64():
+    """fp32 CUDA factors select the fp32 kernels (TTTP loss epilogue, MTTKRP,
+    SGD update); one Poisson SGD step stays within 1e-4 of the fp64 step."""
+    import torch
+    z, t, init = _data()
+    loss = cp.get_loss("poisson")
+    cfg = SolverConfig(rank=3, reg=1e-3, loss="poisson", sample_rate=0.5, step=1e-2)
+    st64 = CompletionState(factors=[f.copy() for f in init], rng=cp.RngState(0))
+    sgd_sweep(t, st64, loss, cfg, cp.RngState(5).child(0))
+    st32 = CompletionState(factors=[torch.from_numpy(f).float().cuda() for f in init],
+                           rng=cp.RngState(0))
+    sgd_sweep(t, st32, cp.get_loss("poisson"), cfg, cp.RngState(5).child(0))
+    for n in range(3):
+        assert st32.factors[n].dtype == torch.float32
+        assert rel(st32.factors[n].double().cpu().numpy(), st64.factors[n]) < 1e-4
