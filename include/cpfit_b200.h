@@ -258,7 +258,8 @@ int cpfit_sgd_update(int dtype, int64_t n, const void *a, const void *grad,
  * NULL) on rhat_0 leaves the residual t - model in canonical order.
  *
  * cpfit_ccd_step: cols[q] = column r of factor q (contiguous fp64, length
- * dims[q]).  With fold_sub / fold_add, rhat is first replaced by
+ * dims[q]); modes q > `mode` must not have been updated yet in this column
+ * (fold_add[q] == cols[q] there, which the pass relies on).  With fold_sub / fold_add, rhat is first replaced by
  * (rhat - prod fold_sub) + prod fold_add at every entry (needs rhat_sorted
  * or an identity-order mode) and written back.  rhat_sorted = 0: a
  * canonical rhat read through the mode permutation, not folded.

@@ -307,7 +307,9 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
         g[u][q] = q != mode ? __ldg(p.cols[q] + iq) : 1.0;
         if constexpr (FOLD) {
           sv[u][q] = p.has_sub ? __ldg(p.sub[q] + iq) : 0.0;
-          av[u][q] = p.has_add ? __ldg(p.add[q] + iq) : 0.0;
+          // modes after this one are not updated yet in this column: their
+          // pre-sweep value is the current one (no second gather)
+          av[u][q] = !p.has_add ? 0.0 : (q > mode ? g[u][q] : __ldg(p.add[q] + iq));
         }
       }
       if constexpr (FOLD) {
