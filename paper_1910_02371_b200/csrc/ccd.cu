@@ -207,7 +207,7 @@ __global__ void ccd_fold_kernel(int order, int64_t nnz, const CcdParams p) {
 #define CCD_FLAT_U 2
 #endif
 #ifndef CCD_FLAT_STEPS
-#define CCD_FLAT_STEPS 8
+#define CCD_FLAT_STEPS 16
 #endif
 constexpr int CCD_FLAT_CHUNK = 32 * CCD_FLAT_U * CCD_FLAT_STEPS;  // entries per warp chunk
 
