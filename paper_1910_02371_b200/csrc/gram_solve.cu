@@ -722,7 +722,7 @@ __device__ __forceinline__ void chol_factor_solve(const T *__restrict__ Gr,
   for (int k = 0; k < RMAX; ++k) {
     const double d = __shfl_sync(0xffffffffu, a[k], k);
     ok = ok && (d > 0.0) && (d < DBL_MAX);
-    const double inv = 1.0 / sqrt(d);
+    const double inv = rsqrt(d);  // MUFU.RSQ64H + Newton: ~1 ulp, no sqrt/div slow paths on the chain
     const double yk = __shfl_sync(0xffffffffu, bj, k) * inv;
     const bool right = lane > k;
     const double ljk = a[k] * inv;                      // L[j][k] on lanes j > k
