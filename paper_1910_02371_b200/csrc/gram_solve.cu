@@ -14,8 +14,8 @@
 //
 // Solve: for R <= 32 one warp per row keeps G + reg I in registers (lane j
 // owns column j) and runs a right-looking Cholesky whose column broadcasts
-// also drive the forward substitution, then back-substitutes with one
-// shuffle per step -- no shared memory, no barriers.  Rows whose Cholesky
+// (warp-uniform shared-memory loads, one __syncwarp per step) also drive the
+// forward substitution, then back-substitutes with one shuffle per step.  Rows whose Cholesky
 // meets a non-positive pivot (and every row when R > 32) go through a
 // shared-memory kernel with a partial-pivoting LU fallback that reports
 // "singular" exactly when LAPACK gesv (np.linalg.solve, kernels.py:259)
@@ -688,6 +688,16 @@ __device__ __forceinline__ void solve_empty_row(const SolveParams<T> &p, int64_t
   if (__any_sync(0xffffffffu, nz) && lane == 0) atomicMin(&p.bad[0], (unsigned long long)row);
 }
 
+// Column broadcast through shared memory (1) or shuffles (0); measured at
+// cfg 3 mode 0 (480k systems, R = 32): shuffles 2.79 ms (96 registers), smem
+// 2.73 ms (132 registers), smem held to 96 registers (5 blocks/SM, a few
+// spilled values) 2.47 ms -- profiles/r1_tuning.md.
+#ifndef CPFIT_CHOL_SMEM
+#define CPFIT_CHOL_SMEM 1
+#endif
+#ifndef CPFIT_SOLVE_MINB
+#define CPFIT_SOLVE_MINB 5
+#endif
 // Register-resident warp Cholesky solve for R <= RMAX <= 32.  Lane j holds
 // column j of (G + reg I) in a[] (G is symmetric: column j is loaded as row
 // entries G[i][j] -- coalesced across lanes) and b_j of the right-hand side
@@ -718,12 +728,34 @@ __device__ __forceinline__ void chol_factor_solve(const T *__restrict__ Gr,
   double bj = lane < R ? (double)__ldg(rh + lane) : 0.0;
   bool ok = true;
   double my_inv = 1.0;  // 1 / L[lane][lane]
+#if CPFIT_CHOL_SMEM
+  // Step k needs A[i][k] (i > k) on every lane; by symmetry of the Schur
+  // complement that is lane i's own a[k]: every lane stores one value and
+  // the column is read back as warp-uniform (broadcast) LDS.128 pairs
+  // instead of two SHFL per element.  Buffers alternate by k parity.
+  __shared__ __align__(16) double col_buf[4][2][32];
+  __shared__ double rhs_buf[4][2];
+  double(&cb)[2][32] = col_buf[(threadIdx.x >> 5) & 3];
+  double(&rb)[2] = rhs_buf[(threadIdx.x >> 5) & 3];
+#endif
 #pragma unroll
   for (int k = 0; k < RMAX; ++k) {
+#if CPFIT_CHOL_SMEM
+    double *c = cb[k & 1];
+    c[lane] = a[k];
+    if (lane == k) rb[k & 1] = bj;
+    __syncwarp();
+    const double d = c[k];
+#else
     const double d = __shfl_sync(0xffffffffu, a[k], k);
+#endif
     ok = ok && (d > 0.0) && (d < DBL_MAX);
     const double inv = rsqrt(d);  // MUFU.RSQ64H + Newton: ~1 ulp, no sqrt/div slow paths on the chain
+#if CPFIT_CHOL_SMEM
+    const double yk = rb[k & 1] * inv;
+#else
     const double yk = __shfl_sync(0xffffffffu, bj, k) * inv;
+#endif
     const bool right = lane > k;
     const double ljk = a[k] * inv;                      // L[j][k] on lanes j > k
     const double sj = right ? ljk * inv : 0.0;          // A[j][k] / d
@@ -731,7 +763,11 @@ __device__ __forceinline__ void chol_factor_solve(const T *__restrict__ Gr,
     if (lane == k) my_inv = inv;
 #pragma unroll
     for (int i = k + 1; i < RMAX; ++i) {
+#if CPFIT_CHOL_SMEM
+      const double ci = c[i];  // A[k][i] = A[i][k] (unscaled)
+#else
       const double ci = __shfl_sync(0xffffffffu, a[i], k);  // A[i][k] (unscaled)
+#endif
       a[i] = fma(-ci, sj, a[i]);  // trailing update of column lane
     }
   }
@@ -757,7 +793,7 @@ __device__ __forceinline__ void chol_factor_solve(const T *__restrict__ Gr,
                                                   double &mine, bool &ok);
 
 template <typename T, int RMAX>
-__global__ void __launch_bounds__(128) solve_reg_kernel(const SolveParams<T> p) {
+__global__ void __launch_bounds__(128, CPFIT_SOLVE_MINB) solve_reg_kernel(const SolveParams<T> p) {
   const int lane = threadIdx.x & 31;
   const int R = p.rank;
   const int64_t wrow = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
