@@ -158,11 +158,11 @@ __global__ void __launch_bounds__(256) tttp_subst_vec_kernel(const SubstParams p
 // Block-diagonal preconditioner, inverted once per GN step: warp per row,
 // lane j holds column j of A = G + shift I (identity-padded to RMAX), and an
 // in-place Gauss-Jordan sweep (no pivoting: A is SPD) leaves A^{-1} in the
-// same layout.  Rows meeting a non-positive pivot are counted in *nbad; the
+// same layout (column broadcasts through shared memory, see below).  Rows meeting a non-positive pivot are counted in *nbad; the
 // caller then keeps the pivoted solve (cpfit_solve_rows) for that mode, so
 // singular systems still fail exactly like np.linalg.solve.
 template <typename T, int RMAX>
-__global__ void __launch_bounds__(128) spd_inverse_kernel(int R, int64_t nrows,
+__global__ void __launch_bounds__(128, 5) spd_inverse_kernel(int R, int64_t nrows,
                                                           const T *__restrict__ gram,
                                                           int64_t gstride, double shift,
                                                           T *__restrict__ inv,
@@ -180,14 +180,25 @@ __global__ void __launch_bounds__(128) spd_inverse_kernel(int R, int64_t nrows,
               : (i == lane ? 1.0 : 0.0);
   }
   bool ok = true;
+  // Column k of the partly swept matrix: A[i][k] = A[k][i] for unswept i
+  // (i >= k) and -A[k][i] for swept i (i < k) -- the sweep keeps the swept
+  // and unswept blocks symmetric and the blocks between them antisymmetric --
+  // so every lane stores its own a[k] and the column is read back as
+  // warp-uniform shared-memory loads (vectorised pairs) instead of 2 x 32
+  // shuffles per step.  Buffers alternate by k parity.
+  __shared__ __align__(16) double col_buf[4][2][32];
+  double(&cb)[2][32] = col_buf[(threadIdx.x >> 5) & 3];
 #pragma unroll
   for (int k = 0; k < RMAX; ++k) {
-    const double piv = __shfl_sync(0xffffffffu, a[k], k);
+    double *cs = cb[k & 1];
+    cs[lane] = a[k];
+    __syncwarp();
+    const double piv = cs[k];
     ok = ok && piv > 0.0 && piv < DBL_MAX;
     const double rp = 1.0 / piv;
     double c[RMAX];
 #pragma unroll
-    for (int i = 0; i < RMAX; ++i) c[i] = __shfl_sync(0xffffffffu, a[i], k);
+    for (int i = 0; i < RMAX; ++i) c[i] = i < k ? -cs[i] : cs[i];
     const double rk = a[k] * rp;
 #pragma unroll
     for (int i = 0; i < RMAX; ++i) {
