@@ -372,6 +372,31 @@ int cpfit_dense_reduce(int dtype, int64_t I, int64_t J, int rank, const void *T,
 int cpfit_khatri_rao(int dtype, int64_t I, int64_t J, int rank, const void *A,
                      const void *B, void *out, void *stream);
 
+/* Dense MTTKRP of an order-3 row-major tensor X (I x J x K), one pass over X
+ * with the Khatri-Rao operand formed in shared memory (csrc/dense_dmma.cu,
+ * csrc/dense_tc.cu):
+ *   mode 0: out[i, r] = sum_jk X[i,j,k] B[j,r] C[k,r]   (einsum('ijk,jr,kr->ir'))
+ *   mode 1: out[j, r] = sum_ik X[i,j,k] A[i,r] C[k,r]
+ *   mode 2: out[k, r] = sum_ij X[i,j,k] A[i,r] B[j,r]
+ * Replaces kernels.mttkrp on a fully observed tensor (kernels.py:46-91; the
+ * reference has no dense type).  F64: FP64 DMMA (parity path);
+ * F32: TF32 tcgen05.mma with TMEM accumulators (TF32 accuracy class).
+ * Factors are row-major (dim x rank); the factor of `mode` may be NULL. */
+int cpfit_dense_mttkrp(int dtype, int64_t I, int64_t J, int64_t K, int rank,
+                       const void *X, const void *A, const void *B, const void *C,
+                       int mode, void *out, void *stream);
+
+/* T[(i*J + j), r] = sum_k X[i,j,k] C[k,r]: the GEMM a dense CP-ALS sweep
+ * shares between modes 0 and 1 (epilogues: cpfit_dense_reduce). */
+int cpfit_dense_xc(int dtype, int64_t I, int64_t J, int64_t K, int rank, const void *X,
+                   const void *C, void *T, void *stream);
+
+/* G[a, b] = prod_f sum_i F_f[i, a] F_f[i, b]: the Hadamard product of the
+ * factors' Gramians, i.e. the shared normal-equation matrix of a dense
+ * CP-ALS mode update (optim.py:192-206 with every entry observed). */
+int cpfit_dense_gram(int dtype, int nfactors, const int64_t *rows, int rank,
+                     const void *const *factors, void *G, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

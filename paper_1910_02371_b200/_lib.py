@@ -42,6 +42,7 @@ SYMBOLS = (
     "cpfit_ccd_gen_update", "cpfit_ccd_gen_model", "cpfit_from_coords",
     "cpfit_tttp_host_async", "cpfit_event_wait", "cpfit_copy_to_host",
     "cpfit_ccsr_spmm", "cpfit_pairwise_tttp", "cpfit_pairwise_fold_sum",
+    "cpfit_dense_mttkrp", "cpfit_dense_xc", "cpfit_dense_gram",
 )
 
 _vp = ctypes.c_void_p
@@ -127,6 +128,10 @@ def load(path: str | None = None):
                              ctypes.POINTER(_i64), _vp],
         "cpfit_dense_reduce": [_int, _i64, _i64, _int, _vp, _vp, _int, _vp, _vp],
         "cpfit_khatri_rao": [_int, _i64, _i64, _int, _vp, _vp, _vp, _vp],
+        "cpfit_dense_mttkrp": [_int, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _int, _vp,
+                               _vp],
+        "cpfit_dense_xc": [_int, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp],
+        "cpfit_dense_gram": [_int, _int, ctypes.POINTER(_i64), _int, _PP, _vp, _vp],
         "cpfit_als_update": [_vp, _int, _int, _int, _vp, _int, _PP, ctypes.c_double, _vp, _vp,
                              _vp, ctypes.POINTER(_i64), _vp],
     }

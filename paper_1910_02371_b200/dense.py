@@ -5,21 +5,20 @@ is ``kernels.mttkrp`` / ``als_sweep`` on a fully observed SparseTensor
 (kernels.py:46-91, optim.py:180-207), against which tests/test_gpu_dense.py
 checks these functions.
 
-einsum('ijk,jr,kr->ir') is computed as one *plain* GEMM plus our epilogue
-kernels (libcpfit_b200, csrc/dense.cu):
+Every contraction runs in this library's own kernels (no cuBLAS):
 
-* modes 0 and 1 share T = X_(IJ x K) @ C (cuBLAS DGEMM on the FP64 tensor
-  pipe), then ``cpfit_dense_reduce`` forms sum_j T[i,j,:] * B[j,:] (mode 0)
-  or sum_i T[i,j,:] * A[i,:] (mode 1);
-* mode 2 is X^T @ KR(A, B) with the Khatri-Rao operand generated by
-  ``cpfit_khatri_rao``.
-
-A CP-ALS sweep therefore costs two GEMMs (2 * 2 I J K R flop), not three.
-The per-mode normal equations share one Gram (the Hadamard product of the
-other factors' R x R Gramians; every row of a dense tensor is fully
-observed) solved for all rows with ``cpfit_solve_rows`` (reg on the diagonal,
-like ``solve_factor``).  ``dtype=torch.float32`` runs the GEMMs in TF32 on
-the tcgen05 tensor cores (fp32 accuracy class, not the fp64 parity path).
+* ``dense_mttkrp(X, F, mode)`` -- einsum('ijk,jr,kr->ir') and its mode-1 /
+  mode-2 analogues as ONE pass over X with the Khatri-Rao operand formed in
+  shared memory (``cpfit_dense_mttkrp``): FP64 DMMA for float64 (the parity
+  path), TF32 ``tcgen05.mma`` with TMEM accumulators for float32.
+* ``dense_als_sweep`` -- one CP-ALS sweep.  Modes 0 and 1 share
+  T = X_(IJ x K) C (``cpfit_dense_xc``, same kernel family; C does not change
+  between them) reduced by ``cpfit_dense_reduce``; mode 2 is one KR pass with
+  the updated A and B.  Two passes over X per sweep instead of three.  The
+  per-mode normal equations share one Gram, the Hadamard product of the
+  other factors' R x R Gramians (``cpfit_dense_gram``; every entry of a dense
+  tensor is observed), solved for all rows by ``cpfit_solve_rows`` (reg on
+  the diagonal, like ``solve_factor``).
 """
 
 from __future__ import annotations
@@ -41,25 +40,68 @@ def _s():
 
 
 def _vp(t):
-    return ctypes.c_void_p(t.data_ptr())
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
 
 
-def _gemm(a, b):
+def _check_dense(X, factors):
     torch = _torch()
-    if a.dtype == torch.float32:
-        prev = torch.backends.cuda.matmul.allow_tf32
-        torch.backends.cuda.matmul.allow_tf32 = True
-        try:
-            return a @ b
-        finally:
-            torch.backends.cuda.matmul.allow_tf32 = prev
-    return a @ b
+    if X.dim() != 3:
+        raise ValueError("dense_mttkrp supports order-3 tensors")
+    if not X.is_cuda:
+        raise ValueError("dense tensors must be CUDA tensors")
+    if X.dtype not in (torch.float64, torch.float32):
+        raise ValueError(f"unsupported dtype {X.dtype}")
+    if len(factors) != 3:
+        raise ValueError("dense_mttkrp needs three factor slots")
+    rank = None
+    for n, f in enumerate(factors):
+        if f is None:
+            continue
+        if f.dim() != 2 or f.shape[0] != X.shape[n]:
+            raise ValueError(f"factor {n} must have shape ({X.shape[n]}, R)")
+        if rank is not None and f.shape[1] != rank:
+            raise ValueError("factor ranks disagree")
+        rank = f.shape[1]
+    if rank is None:
+        raise ValueError("at least one factor is required")
+    return rank
+
+
+def _prep(f, dtype):
+    return None if f is None else f.to(dtype).contiguous()
+
+
+def dense_mttkrp(X, factors, mode: int):
+    """einsum('ijk,jr,kr->ir') (mode 0) and its mode-1 / mode-2 analogues for
+    an order-3 dense CUDA tensor X (float64: FP64 tensor cores; float32:
+    TF32 tcgen05).  The factor in slot ``mode`` is ignored (may be None)."""
+    torch = _torch()
+    rank = _check_dense(X, factors)
+    if mode not in (0, 1, 2):
+        raise ValueError(f"mode {mode} out of range for order-3 tensor")
+    X = X.contiguous()
+    A, B, C = (_prep(f, X.dtype) for f in factors)
+    needed = {0: (B, C), 1: (A, C), 2: (A, B)}[mode]
+    if any(f is None for f in needed):
+        raise ValueError(f"mode {mode} needs the other two factors")
+    I, J, K = X.shape
+    out = torch.empty((X.shape[mode], rank), dtype=X.dtype, device=X.device)
+    _lib.check(_lib.load().cpfit_dense_mttkrp(_dtype_code(X.dtype), I, J, K, rank, _vp(X),
+                                              _vp(A), _vp(B), _vp(C), mode, _vp(out), _s()),
+               "dense_mttkrp")
+    return out
 
 
 def xc_product(X, C):
     """T[i, j, :] = X[i, j, :] @ C   (the GEMM shared by modes 0 and 1)."""
+    torch = _torch()
     I, J, K = X.shape
-    return _gemm(X.reshape(I * J, K), C).reshape(I, J, C.shape[1])
+    C = C.to(X.dtype).contiguous()
+    T = torch.empty((I, J, C.shape[1]), dtype=X.dtype, device=X.device)
+    _lib.check(_lib.load().cpfit_dense_xc(_dtype_code(X.dtype), I, J, K, C.shape[1],
+                                          _vp(X.contiguous()), _vp(C), _vp(T), _s()),
+               "dense_xc")
+    return T
 
 
 def reduce_t(T, W, axis: int):
@@ -82,19 +124,17 @@ def khatri_rao(A, B):
     return out
 
 
-def dense_mttkrp(X, factors, mode: int, T=None):
-    """einsum('ijk,jr,kr->ir') and its mode-1 / mode-2 analogues for an
-    order-3 dense CUDA tensor X (float64, or float32 = TF32 GEMM)."""
-    if X.dim() != 3:
-        raise ValueError("dense_mttkrp supports order-3 tensors")
-    A, B, C = factors
-    if mode in (0, 1):
-        T = xc_product(X, C) if T is None else T
-        return reduce_t(T, B if mode == 0 else A, axis=1 if mode == 0 else 0)
-    if mode == 2:
-        I, J, K = X.shape
-        return _gemm(X.reshape(I * J, K).t(), khatri_rao(A, B))
-    raise ValueError(f"mode {mode} out of range for order-3 tensor")
+def gram_hadamard(factors):
+    """G = prod_f F_f^T F_f (elementwise), R x R, on the device."""
+    torch = _torch()
+    fs = [f.contiguous() for f in factors]
+    rank = fs[0].shape[1]
+    G = torch.empty((rank, rank), dtype=fs[0].dtype, device=fs[0].device)
+    rows = (ctypes.c_int64 * len(fs))(*[f.shape[0] for f in fs])
+    _lib.check(_lib.load().cpfit_dense_gram(_dtype_code(fs[0].dtype), len(fs), rows, rank,
+                                            _lib.ptr_array([f.data_ptr() for f in fs]),
+                                            _vp(G), _s()), "dense_gram")
+    return G
 
 
 def solve_shared(G, rhs, reg: float):
@@ -116,11 +156,12 @@ def dense_als_sweep(X, factors, reg: float):
     """One CP-ALS sweep (modes in order, reg on the diagonal as in the
     reference's least-squares als_sweep, optim.py:192-206); factors are CUDA
     tensors, replaced in the list."""
-    A, B, C = factors
-    T = xc_product(X, C)  # C is unchanged while modes 0 and 1 update
+    _check_dense(X, factors)
+    X = X.contiguous()
+    T = xc_product(X, factors[2])  # C is unchanged while modes 0 and 1 update
     for mode in range(3):
         others = [factors[n] for n in range(3) if n != mode]
-        G = (others[0].t() @ others[0]) * (others[1].t() @ others[1])
+        G = gram_hadamard(others)
         if mode == 0:
             M = reduce_t(T, factors[1], axis=1)
         elif mode == 1:
@@ -131,4 +172,5 @@ def dense_als_sweep(X, factors, reg: float):
     return factors
 
 
-__all__ = ["dense_mttkrp", "dense_als_sweep", "khatri_rao", "solve_shared", "xc_product"]
+__all__ = ["dense_mttkrp", "dense_als_sweep", "gram_hadamard", "khatri_rao", "solve_shared",
+           "xc_product"]
