@@ -42,9 +42,6 @@ namespace cpfit {
 namespace dmma {
 
 constexpr int KC = 32;      // reduction values per stage
-constexpr int NT = 64;      // output columns per CTA
-constexpr int BP = 72;      // KR tile pitch (doubles): rows 0..3 of a B fragment hit 2 bank groups
-constexpr int STAGES = 3;
 
 struct Args {
   int mode;
@@ -61,10 +58,17 @@ struct Args {
   int use_tma;
 };
 
-template <int TM>
+// WN = warps along N: 2 -> 64-column CTA tile, 8 warps, 3 stages, 1 CTA/SM;
+//                     1 -> 32-column CTA tile, 4 warps, 2 stages, 2 CTAs/SM
+//                          (one CTA's per-stage barrier is covered by the other's math)
+template <int TM, int WN>
 struct Cfg {
   static constexpr int MT = 32 * TM;   // 4 warps along M, 8 TM rows each
-  static constexpr int THREADS = 256;
+  static constexpr int NT = 32 * WN;
+  static constexpr int THREADS = 128 * WN;
+  static constexpr int STAGES = WN == 2 ? 3 : 2;
+  static constexpr int MINB = WN == 2 ? 1 : 2;
+  static constexpr int BP = NT + 8;    // KR tile pitch: rows 0..3 of a B fragment hit 2 bank groups
   static constexpr int A_DBL = MT * KC;
   static constexpr int B_DBL = KC * BP;
   static constexpr int STAGE_BYTES = ((A_DBL + B_DBL) * 8 + 1023) / 1024 * 1024;
@@ -101,10 +105,11 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int TM, bool MN>
-__global__ void __launch_bounds__(256, 1)
+template <int TM, int WN, bool MN>
+__global__ void __launch_bounds__(128 * WN, (WN == 2 ? 1 : 2))
     dense_dmma_kernel(const __grid_constant__ CUtensorMap tmap, const Args a) {
-  typedef Cfg<TM> C;
+  typedef Cfg<TM, WN> C;
+  constexpr int STAGES = C::STAGES, NT = C::NT, BP = C::BP;
   constexpr int MT = C::MT;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned base by pointer arithmetic on the shared array (keeps the
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(256, 1)
   // read as 16-byte vectors when the rank allows; the F1 row (fixed p) is
   // re-read only when p changes.
   constexpr bool builder = true;
-  const int bq = tid >> 3, bn = (tid & 7) * 8;
+  const int bq = tid / (NT / 8), bn = (tid % (NT / 8)) * 8;
   const bool vec = (a.R % 2 == 0) && (((uintptr_t)a.F2 | (uintptr_t)a.F1) % 16 == 0);
   double f1r[8], f2r[8];
   int64_t f1_p = -1;
@@ -302,49 +307,65 @@ int split_sum_f32(const float *part, int nsplit, int64_t n, float *out, cudaStre
   return CPFIT_OK;
 }
 
-// G[a, b] = prod_f sum_i F_f[i, a] F_f[i, b]  (fixed summation order)
+// G[a, b] = prod_f sum_i F_f[i, a] F_f[i, b]: one CTA per row a, thread (slice, b)
+// sums its row slice, slices combined in order (deterministic)
 template <typename T>
 __global__ void dense_gram_kernel(int nf, CpfitDims rows, int R, CpfitCoordPtrs<T> F,
                                   T *__restrict__ G) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= R * R) return;
-  const int ra = e / R, rb = e % R;
+  extern __shared__ double red[];
+  const int a = blockIdx.x, t = threadIdx.x;
+  const int S = blockDim.x / R, b = t % R, sl = t / R;
   double prod = 1.0;
   for (int f = 0; f < nf; ++f) {
     const T *p = F.p[f];
+    const int64_t n = rows.d[f], per = (n + S - 1) / S;
     double acc = 0.0;
-    for (int64_t i = 0; i < rows.d[f]; ++i)
-      acc += (double)__ldg(p + i * R + ra) * (double)__ldg(p + i * R + rb);
-    prod *= acc;
+    if (sl < S) {
+      const int64_t i1 = min(n, (sl + 1) * per);
+      for (int64_t i = sl * per; i < i1; ++i)
+        acc += (double)__ldg(p + i * R + a) * (double)__ldg(p + i * R + b);
+    }
+    red[t] = acc;
+    __syncthreads();
+    if (sl == 0) {
+      double tot = red[b];
+      for (int k = 1; k < S; ++k) tot += red[k * R + b];
+      prod *= tot;
+    }
+    __syncthreads();
   }
-  G[e] = (T)prod;
+  if (sl == 0) G[a * R + b] = (T)prod;
 }
 
 namespace dmma {
 
 struct Plan {
-  int tm;
+  int tm, wn;
   int64_t n_mt, nsplit, per_split, n_nt;
 };
 
-inline Plan plan(int64_t rows, int64_t nchunks, int R) {
+inline Plan plan(int64_t rows, int64_t nchunks, int R, int wn) {
   const int sms = num_sms();
+  const int per_sm = wn == 2 ? 1 : 2;   // resident CTAs per SM
+  const int NT = 32 * wn;
   Plan best{};
   double best_cost = -1;
   for (int tm = 4; tm <= 5; ++tm) {
     const int MT = 32 * tm;
     Plan p;
     p.tm = tm;
+    p.wn = wn;
     p.n_mt = (rows + MT - 1) / MT;
     p.n_nt = (R + NT - 1) / NT;
     const int64_t tiles = p.n_mt * p.n_nt;
-    int64_t ns = tiles >= sms ? 1 : sms / tiles;
+    const int64_t slots = (int64_t)sms * per_sm;
+    int64_t ns = tiles >= slots ? 1 : slots / tiles;
     if (ns > nchunks) ns = nchunks;
     if (ns < 1) ns = 1;
     p.per_split = (nchunks + ns - 1) / ns;
     p.nsplit = (nchunks + p.per_split - 1) / p.per_split;
     const int64_t ctas = tiles * p.nsplit;
-    const double cost = (double)((ctas + sms - 1) / sms) * (double)p.per_split * MT;
+    const double cost = (double)((ctas + slots - 1) / slots) * (double)p.per_split * MT;
     if (best_cost < 0 || cost < best_cost) {
       best_cost = cost;
       best = p;
@@ -353,18 +374,36 @@ inline Plan plan(int64_t rows, int64_t nchunks, int R) {
   return best;
 }
 
-template <int TM, bool MN>
+template <int TM, int WN, bool MN>
 int launch(const CUtensorMap &map, const Args &a, const Plan &p, cudaStream_t s) {
+  typedef Cfg<TM, WN> C;
   static bool configured = false;
   if (!configured) {
-    CPFIT_CUDA(cudaFuncSetAttribute(dense_dmma_kernel<TM, MN>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<TM>::SMEM));
+    CPFIT_CUDA(cudaFuncSetAttribute(dense_dmma_kernel<TM, WN, MN>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     configured = true;
   }
   dim3 grid((unsigned)p.n_mt, (unsigned)p.nsplit, (unsigned)p.n_nt);
-  dense_dmma_kernel<TM, MN><<<grid, Cfg<TM>::THREADS, Cfg<TM>::SMEM, s>>>(map, a);
+  dense_dmma_kernel<TM, WN, MN><<<grid, C::THREADS, C::SMEM, s>>>(map, a);
   CPFIT_LAUNCH_CHECK("dense_dmma_kernel");
   return CPFIT_OK;
+}
+
+template <int WN>
+int launch_wn(const CUtensorMap &map, const Args &a, const Plan &p, cudaStream_t s) {
+  const bool mn = a.mode == 2;
+  if (p.tm == 4) return mn ? launch<4, WN, true>(map, a, p, s) : launch<4, WN, false>(map, a, p, s);
+  return mn ? launch<5, WN, true>(map, a, p, s) : launch<5, WN, false>(map, a, p, s);
+}
+
+// CTA shape (measurement knob; default: the faster one on B200)
+inline int cta_wn() {
+  static int wn = 0;
+  if (!wn) {
+    const char *e = getenv("CPFIT_DMMA_WN");
+    wn = (e && atoi(e) == 2) ? 2 : 1;  // 1: 2 CTAs/SM (0.81-0.83 of cuBLAS DGEMM vs 0.79-0.80)
+  }
+  return wn;
 }
 
 // Runs one dense KR-GEMM (modes 0..2) or the X.C GEMM (mode 3) in fp64.
@@ -388,7 +427,7 @@ inline int run(int mode, int64_t I, int64_t J, int64_t K, int R, const double *X
   }
   a.nqc = (a.nq + KC - 1) / KC;
   a.nchunks = np * a.nqc;
-  Plan p = plan(a.rows, a.nchunks, R);
+  Plan p = plan(a.rows, a.nchunks, R, cta_wn());
   a.per_split = p.per_split;
   const int MT = 32 * p.tm;
 
@@ -418,10 +457,10 @@ inline int run(int mode, int64_t I, int64_t J, int64_t K, int R, const double *X
   } else {
     a.out = out;
   }
-  if (p.tm == 4)
-    CPFIT_TRY((mode == 2 ? launch<4, true>(map, a, p, s) : launch<4, false>(map, a, p, s)));
+  if (p.wn == 2)
+    CPFIT_TRY(launch_wn<2>(map, a, p, s));
   else
-    CPFIT_TRY((mode == 2 ? launch<5, true>(map, a, p, s) : launch<5, false>(map, a, p, s)));
+    CPFIT_TRY(launch_wn<1>(map, a, p, s));
   if (p.nsplit > 1) {
     const int64_t n = a.rows * R;
     dense_split_sum<double, double><<<grid_for(n, 256), 256, 0, s>>>(part.ptr, (int)p.nsplit, n,
@@ -493,16 +532,21 @@ int cpfit_dense_gram(int dtype, int nfactors, const int64_t *rows, int rank,
   CpfitDims d{};
   for (int f = 0; f < nfactors; ++f) d.d[f] = rows[f];
   cudaStream_t s = (cudaStream_t)stream;
-  const int total = rank * rank;
-  const unsigned blocks = (unsigned)((total + 127) / 128);
+  if (rank > 1024) {
+    set_error("dense_gram: rank %d > 1024", rank);
+    return CPFIT_EINVAL;
+  }
+  const int S = 256 / rank > 0 ? 256 / rank : 1;
+  const int threads = rank * S;
+  const size_t shm = (size_t)threads * sizeof(double);
   if (dtype == CPFIT_F64) {
     CpfitCoordPtrs<double> F{};
     for (int f = 0; f < nfactors; ++f) F.p[f] = (const double *)factors[f];
-    dense_gram_kernel<double><<<blocks, 128, 0, s>>>(nfactors, d, rank, F, (double *)G);
+    dense_gram_kernel<double><<<rank, threads, shm, s>>>(nfactors, d, rank, F, (double *)G);
   } else if (dtype == CPFIT_F32) {
     CpfitCoordPtrs<float> F{};
     for (int f = 0; f < nfactors; ++f) F.p[f] = (const float *)factors[f];
-    dense_gram_kernel<float><<<blocks, 128, 0, s>>>(nfactors, d, rank, F, (float *)G);
+    dense_gram_kernel<float><<<rank, threads, shm, s>>>(nfactors, d, rank, F, (float *)G);
   } else {
     set_error("unknown dtype %d", dtype);
     return CPFIT_EINVAL;

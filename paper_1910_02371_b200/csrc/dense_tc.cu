@@ -229,11 +229,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int64_t p = c / a.nqc, q0 = (c % a.nqc) * KC;
       const float f1 = (a.F1 && colok) ? __ldg(a.F1 + p * a.R + col) : 1.f;
       float v[KC];
+#ifdef CPFIT_TC_NOBUILD
 #pragma unroll
-      for (int j = 0; j < KC; ++j) {
-        const int64_t q = q0 + j;
-        v[j] = (colok && q < a.nq) ? __ldg(a.F2 + q * a.R + col) : 0.f;
+      for (int j = 0; j < KC; ++j) v[j] = 0.f;
+#else
+      if (colok && q0 + KC <= a.nq) {  // whole chunk inside: unpredicated strided loads
+        const float *src = a.F2 + q0 * a.R + col;
+#pragma unroll
+        for (int j = 0; j < KC; ++j) v[j] = __ldg(src + j * a.R);
+      } else {
+#pragma unroll
+        for (int j = 0; j < KC; ++j) {
+          const int64_t q = q0 + j;
+          v[j] = (colok && q < a.nq) ? __ldg(a.F2 + q * a.R + col) : 0.f;
+        }
       }
+#endif
       if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
       unsigned char *dst = stage_b(s) + r * 128;
 #pragma unroll

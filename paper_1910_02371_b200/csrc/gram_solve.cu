@@ -1046,6 +1046,113 @@ static int launch_solve_smem(const SolveParams<T> &p, int rank, int64_t nrows, c
   return CPFIT_OK;
 }
 
+// ---- one shared SPD matrix for every row (dense CP-ALS: G = Hadamard of the
+// other factors' Gramians, every entry observed) --------------------------------
+// (G + reg I)^-1 once: right-looking Cholesky in shared memory by one CTA, then
+// thread j solves L L^T x = e_j in place in column j of Ainv.  *bad = 1 when a
+// pivot is not positive (the caller then takes the per-row path, whose
+// LU fallback carries the reference's singular-row semantics).
+template <typename T>
+__global__ void shared_spd_inverse(int R, const T *__restrict__ G, double reg,
+                                   double *__restrict__ Ainv, int *__restrict__ bad) {
+  extern __shared__ double Ls[];
+  __shared__ int fail;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < R * R; e += nt) {
+    const int i = e / R, j = e % R;
+    Ls[e] = (double)G[e] + (i == j ? reg : 0.0);
+  }
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  for (int k = 0; k < R; ++k) {
+    if (tid == 0) {
+      const double d = Ls[k * R + k];
+      if (!(d > 0.0) || !isfinite(d)) fail = 1;
+      else Ls[k * R + k] = sqrt(d);
+    }
+    __syncthreads();
+    if (fail) break;
+    const double piv = Ls[k * R + k];
+    for (int i = k + 1 + tid; i < R; i += nt) Ls[i * R + k] /= piv;
+    __syncthreads();
+    const int w = R - k - 1;
+    for (int e = tid; e < w * w; e += nt) {
+      const int i = k + 1 + e / w, j = k + 1 + e % w;
+      if (j <= i) Ls[i * R + j] -= Ls[i * R + k] * Ls[j * R + k];
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) *bad = 1;
+    return;
+  }
+  double *Y = Ls + R * R;  // column j of the inverse, solved in shared memory by thread j
+  for (int j = tid; j < R; j += nt) {
+    for (int i = 0; i < R; ++i) {  // L y = e_j
+      double acc = (i == j) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) acc -= Ls[i * R + k] * Y[k * R + j];
+      Y[i * R + j] = acc / Ls[i * R + i];
+    }
+    for (int i = R - 1; i >= 0; --i) {  // L^T x = y, in place
+      double acc = Y[i * R + j];
+      for (int k = i + 1; k < R; ++k) acc -= Ls[k * R + i] * Y[k * R + j];
+      Y[i * R + j] = acc / Ls[i * R + i];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < R * R; e += nt) Ainv[e] = Y[e];
+}
+
+// x[i, r] = sum_k rhs[i, k] Ainv[k, r]
+template <typename T>
+__global__ void shared_spd_apply(int64_t n, int R, const T *__restrict__ rhs,
+                                 const double *__restrict__ Ainv, T *__restrict__ x) {
+  const int64_t total = n * R;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = o / R;
+    const int r = (int)(o - i * R);
+    const T *b = rhs + i * R;
+    double acc = 0.0;
+    for (int k = 0; k < R; ++k) acc += (double)b[k] * Ainv[k * R + r];
+    x[o] = (T)acc;
+  }
+}
+
+// returns 1 when the shared path solved everything, 0 to fall back
+template <typename T>
+static int solve_shared_spd(int64_t n, int R, const T *gram, const T *rhs, double reg, T *x,
+                            cudaStream_t s, int *status) {
+  *status = CPFIT_OK;
+  if (R > 112 || n < 2) return 0;  // L and the inverse both live in shared memory
+  const size_t shm = 2 * (size_t)R * R * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(shared_spd_inverse<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         2 * 112 * 112 * (int)sizeof(double));
+    configured = true;
+  }
+  Scratch<double> inv(s);
+  Scratch<int> bad(s);
+  if ((*status = inv.alloc((size_t)R * R)) != CPFIT_OK) return 1;
+  if ((*status = bad.alloc(1)) != CPFIT_OK) return 1;
+  cudaMemsetAsync(bad.ptr, 0, sizeof(int), s);
+  const int threads = R * R >= 256 ? 256 : 64;
+  shared_spd_inverse<T><<<1, threads, shm, s>>>(R, gram, reg, inv.ptr, bad.ptr);
+  int h = 0;
+  cudaMemcpyAsync(&h, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    *status = cuda_status(e, "shared_spd_inverse");
+    return 1;
+  }
+  if (h) return 0;
+  shared_spd_apply<T><<<grid_for(n * R, 256), 256, 0, s>>>(n, R, rhs, inv.ptr, x);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) *status = cuda_status(e, "shared_spd_apply");
+  return 1;
+}
+
 template <typename T>
 static int run_solve_rows(int mode, int64_t dim, const int64_t *offsets, int rank, const T *gram,
                           int64_t gstride, const T *rhs, double reg, T *x, int64_t *bad_row,
@@ -1206,6 +1313,17 @@ int cpfit_solve_rows(int dtype, int rank, int64_t nrows, const void *gram, int64
   if (nrows == 0) return CPFIT_OK;
   cudaStream_t s = (cudaStream_t)stream;
   int64_t dummy = -1;
+  if (gram_stride == 0 && (dtype == CPFIT_F64 || dtype == CPFIT_F32)) {
+    // one shared G: factor and invert it once (falls through when not SPD)
+    int st = CPFIT_OK;
+    const int done =
+        dtype == CPFIT_F64
+            ? solve_shared_spd<double>(nrows, rank, (const double *)gram, (const double *)rhs, reg,
+                                       (double *)x_out, s, &st)
+            : solve_shared_spd<float>(nrows, rank, (const float *)gram, (const float *)rhs, reg,
+                                      (float *)x_out, s, &st);
+    if (done) return st;
+  }
   if (dtype == CPFIT_F64)
     return run_solve_rows<double>(-1, nrows, nullptr, rank, (const double *)gram, gram_stride,
                                   (const double *)rhs, reg, (double *)x_out,

@@ -152,3 +152,20 @@ def test_dense_rejects_bad_arguments():
         dense_mttkrp(Xd, [f[0], f[1][:, :2], f[2]], 0)
     with pytest.raises(ValueError):
         dense_mttkrp(Xd, [f[0], None, f[2]], 0)
+
+
+def test_dense_shared_solve_and_singular_fallback():
+    torch = _torch()
+    from paper_1910_02371_b200.dense import solve_shared
+    from paper_1910_02371_b200.exceptions import NumericalError
+    rng = np.random.default_rng(2)
+    B = rng.standard_normal((50, 24))
+    G = B.T @ B
+    rhs = rng.standard_normal((77, 24))
+    x = solve_shared(torch.from_numpy(G).cuda(), torch.from_numpy(rhs).cuda(), 1e-3).cpu().numpy()
+    ref = np.linalg.solve(G + 1e-3 * np.eye(24), rhs.T).T
+    assert rel(x, ref) < 1e-12
+    # not SPD -> the per-row path with the reference's singular-row semantics
+    with pytest.raises(NumericalError):
+        solve_shared(torch.zeros((24, 24), dtype=torch.float64, device="cuda"),
+                     torch.from_numpy(rhs).cuda(), 0.0)

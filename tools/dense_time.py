@@ -36,6 +36,13 @@ out["f64_tflops"] = [flop / (t * 1e-3) / 1e12 for t in out["f64_ms"]]
 out["xc_ms"] = timed(lambda: DN.xc_product(X, F[2]))
 Fs = [f.clone() for f in F]
 out["als_sweep_ms"] = timed(lambda: DN.dense_als_sweep(X, Fs, 1e-5), reps=3)
+T = DN.xc_product(X, F[2])
+out["reduce_ms"] = [timed(lambda: DN.reduce_t(T, F[1], 1)), timed(lambda: DN.reduce_t(T, F[0], 0))]
+out["gram_ms"] = timed(lambda: DN.gram_hadamard(F[:2]))
+G = DN.gram_hadamard(F[:2])
+M = DN.dense_mttkrp(X, F, 0)
+out["solve_ms"] = timed(lambda: DN.solve_shared(G, M, 1e-5))
+del T
 a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
 pk = timed(lambda: a @ a)
 out["cublas_dgemm_tflops"] = 2 * 8192 ** 3 / (pk * 1e-3) / 1e12
