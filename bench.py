@@ -495,7 +495,8 @@ def ingest_section(dev, reps=3):
     import torch
 
     from paper_1910_02371_b200 import synth
-    from paper_1910_02371_b200.core import _merge_sorted, from_coords_device, linearize_many
+    from oracle import oracle as O
+    from paper_1910_02371_b200.core import from_coords_device
     shape, keys, values, _ = synth.cfg2()
     rng = np.random.default_rng(77)
     dup = rng.integers(0, keys.size, keys.size // 10)
@@ -522,9 +523,9 @@ def ingest_section(dev, reps=3):
     out["device_ms"] = float(np.median(times))
     out["device_entries_per_s"] = allk.size / (out["device_ms"] * 1e-3)
     t0 = time.perf_counter()
-    ref = _merge_sorted(shape, linearize_many(coords, shape), allv)
+    ref = O.from_coords(coords, allv, shape)
     out["host_numpy_s"] = time.perf_counter() - t0
-    out["host_what"] = "numpy restatement of core.py:208-231 on one host core"
+    out["host_what"] = "oracle numpy restatement of core.py:208-231 on one host core"
     ok = t.nnz == ref.nnz and np.array_equal(t.keys, ref.keys) and \
         np.array_equal(t.values, ref.values)
     out["bit_identical_to_numpy"] = bool(ok)

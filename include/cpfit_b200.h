@@ -337,7 +337,9 @@ int cpfit_loss_eval(int loss, int dtype, int64_t n, const void *t, const void *m
 
 /* Inner-Newton CCD++ column step for generalized losses (optim.py:269-294),
  * fp64, canonical entry order.  cpfit_ccd_gen_weights: part_e = prod_{p !=
- * mode} cols[p][i_p(e)], w1 = part * dphi(t, model), w2 = part^2 * d2phi;
+ * mode} cols[p][i_p(e)], w1 = part * dphi(t, model), w2 = part^2 * d2phi
+ * (loss 2: a user-registered loss whose dphi / d2phi the caller evaluated
+ * on the host -- passed in place of t / model);
  * the row sums num / den come from cpfit_mttkrp (R = 1, unit columns);
  * cpfit_ccd_gen_update: delta = -(num + 2 reg col) / (den + 2 reg) where the
  * denominator is > 0, else 0, col += delta; cpfit_ccd_gen_model:

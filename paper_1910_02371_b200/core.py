@@ -14,8 +14,9 @@ never re-sort.  Values live on the device per dtype; host ``keys`` /
 ``values`` are materialised lazily for device-born tensors (samples, kernel
 outputs).
 
-Host-side helpers (linearize on a tuple, ingest sorting/duplicate merging in
-``from_coords``, synthetic generators) stay numpy, as in the reference.
+Ingest (``from_coords`` / ``build_tensor``: linearize, stable sort,
+duplicate merge) runs on the device too; only scalar helpers (linearize on a
+tuple) and the seeded synthetic generators stay on the host.
 """
 
 from __future__ import annotations
@@ -111,8 +112,11 @@ class _CudaArray:
 def device_view(ptr: int, n: int, typestr: str, owner=None):
     """torch view of library-owned memory (keep ``owner`` alive while used)."""
     torch = _torch()
-    t = torch.as_tensor(_CudaArray(ptr, n, typestr), device=cuda_device())
-    return t
+    arr = _CudaArray(ptr, n, typestr)
+    # torch keeps the interface object alive as long as the tensor: hanging
+    # the owner on it ties the pattern's lifetime to every view of its memory
+    arr._owner = owner
+    return torch.as_tensor(arr, device=cuda_device())
 
 
 class DevicePattern:
@@ -493,34 +497,28 @@ class SparseTensor:
 
 
 def build_tensor(entries, shape) -> SparseTensor:
-    """core.py:192-205: unsorted ((coords...), value) pairs, duplicates summed."""
+    """core.py:192-205: unsorted ((coords...), value) pairs, duplicates summed
+    -- through the device ingest like from_coords."""
     shape = check_shape(shape)
     if not entries:
         return SparseTensor(shape, np.empty(0, np.uint64), np.empty(0))
-    keys = np.fromiter((linearize(c, shape) for c, _ in entries), dtype=np.uint64,
-                       count=len(entries))
+    for c, _ in entries:  # per-entry validation with the reference's messages
+        linearize(c, shape)
+    cols = np.array([tuple(c) for c, _ in entries], dtype=np.int64).reshape(len(entries), -1)
     values = np.fromiter((v for _, v in entries), dtype=np.float64, count=len(entries))
-    return _merge_sorted(shape, keys, values)
+    return from_coords_device([cols[:, n] for n in range(len(shape))], values, shape)
 
 
 def from_coords(coord_arrays, values, shape) -> SparseTensor:
     """core.py:208-218: per-mode coordinate arrays, duplicates summed.
 
-    With a CUDA device the whole ingest runs there (cpfit_from_coords:
-    linearize, stable radix sort, duplicate merge in numpy's reduceat order;
-    bit-identical keys and values); numpy inputs are uploaded first.  Without
-    one (CPU-only host-logic tests) the numpy restatement below is used."""
+    The whole ingest runs on the device (cpfit_from_coords: linearize, stable
+    radix sort, duplicate merge in numpy's reduceat order; bit-identical keys
+    and values); numpy inputs are uploaded first.  No CPU path."""
     shape = check_shape(shape)
     if len(coord_arrays) != len(shape):
         raise ValueError("one coordinate array per mode required")
-    torch = _torch()
-    if torch.cuda.is_available():
-        return from_coords_device(coord_arrays, values, shape)
-    values = np.ascontiguousarray(values, dtype=np.float64)
-    keys = linearize_many(coord_arrays, shape)
-    if keys.shape != values.shape:
-        raise ValueError("coordinate arrays and values must have equal length")
-    return _merge_sorted(shape, keys, values)
+    return from_coords_device(coord_arrays, values, shape)
 
 
 def from_coords_device(coord_arrays, values, shape) -> SparseTensor:
@@ -573,20 +571,6 @@ def from_coords_device(coord_arrays, values, shape) -> SparseTensor:
     _lib.check(st, "from_coords")
     m = nnz.value
     return SparseTensor.from_device(shape, keys[:m], out[:m])
-
-
-def _merge_sorted(shape, keys, values) -> SparseTensor:
-    """core.py:221-231: stable key sort, duplicates summed in stable order."""
-    if keys.size == 0:
-        return SparseTensor(shape, keys, values, validate=False)
-    order = np.argsort(keys, kind="stable")
-    keys = keys[order]
-    values = values[order]
-    starts = np.flatnonzero(np.concatenate(([True], keys[1:] != keys[:-1])))
-    if starts.size != keys.size:
-        values = np.add.reduceat(values, starts)
-        keys = keys[starts]
-    return SparseTensor(shape, keys, values, validate=False)
 
 
 def counting_sort_by_mode(t: SparseTensor, mode: int):

@@ -60,7 +60,12 @@ __global__ void ccd_gen_weights_kernel(int order, int mode, int loss, int64_t n,
         part = __dmul_rn(part, __ldg(cols.col[q] + __ldg(cols.idx[q] + e)));
       }
       double f, d1, d2;
-      cl = loss_eval1(loss, t[e], model[e], f, d1, d2);
+      if (loss == 2) {  // derivatives evaluated by the caller (user-registered loss)
+        d1 = t[e];
+        d2 = model[e];
+      } else {
+        cl = loss_eval1(loss, t[e], model[e], f, d1, d2);
+      }
       w1[e] = __dmul_rn(part, d1);
       w2[e] = __dmul_rn(__dmul_rn(part, part), d2);
       part_out[e] = part;
@@ -145,7 +150,7 @@ int cpfit_ccd_gen_weights(cpfit_pattern *pt, int mode, int loss, const double *c
                           const double *t, const double *model, double *w1, double *w2,
                           double *part, int64_t *clamped, void *stream) {
   if (!pt || mode < 0 || mode >= pt->order) { set_error("mode %d out of range", mode); return CPFIT_EINVAL; }
-  if (loss < 0 || loss > 1) { set_error("unknown loss id %d", loss); return CPFIT_EINVAL; }
+  if (loss < 0 || loss > 2) { set_error("unknown loss id %d", loss); return CPFIT_EINVAL; }
   cudaStream_t s = (cudaStream_t)stream;
   if (clamped) *clamped = 0;
   if (pt->nnz == 0) return CPFIT_OK;

@@ -458,46 +458,19 @@ def ccd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
         _ccd_ls_device(t, F, cfg.reg)
         _write_back(state.factors, F)
         return
-    if loss.device_id is not None:
-        F = _to_dev_factors(state.factors, _torch().float64)
-        _ccd_generalized_device(t, F, loss, cfg)
-        _write_back(state.factors, F)
-        return
-    # user-registered loss: inner Newton per column with its host callables
-    coords = t.coords()
-    factors = [_as_np(f).copy() for f in state.factors]
-    order, rank = t.order, factors[0].shape[1]
-    from .core import model_values
-    model = model_values(factors, coords)
-    for r in range(rank):
-        cols = [factors[n][:, r] for n in range(order)]
-        for mode in range(order):
-            partial = np.ones(t.nnz)
-            for p in range(order):
-                if p != mode:
-                    partial = partial * cols[p][coords[p]]
-            for inner in range(cfg.inner_max):
-                phi1 = loss.dphi(t.values, model)
-                phi2 = loss.d2phi(t.values, model)
-                num = np.bincount(coords[mode], weights=partial * phi1, minlength=t.shape[mode])
-                num += 2.0 * cfg.reg * cols[mode]
-                den = np.bincount(coords[mode], weights=partial * partial * phi2,
-                                  minlength=t.shape[mode])
-                den += 2.0 * cfg.reg
-                delta = np.where(den > 0.0, -num / np.where(den > 0.0, den, 1.0), 0.0)
-                cols[mode][:] += delta
-                model = model + partial * delta[coords[mode]]
-                rel = np.linalg.norm(delta) / max(np.linalg.norm(cols[mode]), _TINY)
-                if rel < cfg.inner_tol:
-                    break
-    for n in range(order):
-        state.factors[n] = _like(state.factors[n], factors[n])
+    # built-in losses evaluate dphi / d2phi on the device; a user-registered
+    # loss runs the same device sweep with its host callables
+    F = _to_dev_factors(state.factors, _torch().float64)
+    _ccd_generalized_device(t, F, loss, cfg)
+    _write_back(state.factors, F)
 
 
 def _ccd_generalized_device(t: SparseTensor, F, loss: LossFunction, cfg: SolverConfig):
     """Inner-Newton CCD++ sweep of a built-in loss on device factors
     (optim.py:269-294): per (r, mode, inner step) the weights part * dphi and
-    part^2 * d2phi at the current model (cpfit_ccd_gen_weights), their row
+    part^2 * d2phi at the current model (cpfit_ccd_gen_weights; for a
+    user-registered loss its dphi / d2phi callables run on the model values
+    copied to the host, as the reference evaluates them), their row
     sums (two R = 1 MTTKRPs against unit columns), the damped-free Newton
     column update and the model update; the stopping test reads two
     fixed-order device norms."""
@@ -523,6 +496,9 @@ def _ccd_generalized_device(t: SparseTensor, F, loss: LossFunction, cfg: SolverC
     deltas = [torch.empty(d, dtype=f64, device=dev) for d in t.shape]
     clamped = ctypes.c_int64(0)
     count = loss.device_id == 1
+    user = loss.device_id is None
+    lid = 2 if user else int(loss.device_id)
+    t_host = t.values if user else None
     for r in range(rank):
         keep, ptrs = _ccd_col_ptrs(cols, r)
         for mode in range(order):
@@ -531,9 +507,16 @@ def _ccd_generalized_device(t: SparseTensor, F, loss: LossFunction, cfg: SolverC
             den = torch.zeros((t.shape[mode], 1), dtype=f64, device=dev)
             for inner in range(cfg.inner_max):
                 if t.nnz:
+                    a1, a2 = tv, model
+                    if user:
+                        m_host = model.cpu().numpy()
+                        a1 = torch.from_numpy(np.ascontiguousarray(
+                            loss.dphi(t_host, m_host), dtype=np.float64)).to(dev)
+                        a2 = torch.from_numpy(np.ascontiguousarray(
+                            loss.d2phi(t_host, m_host), dtype=np.float64)).to(dev)
                     _lib.check(L.cpfit_ccd_gen_weights(
-                        pat.handle, mode, int(loss.device_id), ptrs,
-                        ctypes.c_void_p(tv.data_ptr()), ctypes.c_void_p(model.data_ptr()),
+                        pat.handle, mode, lid, ptrs,
+                        ctypes.c_void_p(a1.data_ptr()), ctypes.c_void_p(a2.data_ptr()),
                         ctypes.c_void_p(w1.data_ptr()), ctypes.c_void_p(w2.data_ptr()),
                         ctypes.c_void_p(part.data_ptr()),
                         ctypes.byref(clamped) if count else None, _stream()), "ccd_gen_weights")

@@ -33,7 +33,6 @@ Fixtures:
                         (canonical and eager, k = 2 / 3, P = 5), ttm,
                         pairwise_mttkrp (orders 3 / 4), pairwise_tttp (R up
                         to 20, absent factors)
-  estimator.npz      -- CPCompletion fit / predict / score (coordinate input)
   cli.npz            -- `cpfit gen` output bytes and `cpfit run --deterministic`
                         trace CSVs (als / ccd / sgd / gn, ls and poisson)
   second_order.npz   -- hessian_matvec (ls/poisson x gauss_newton/newton),
@@ -518,22 +517,6 @@ def cli():
     np.savez_compressed(os.path.join(HERE, "cli.npz"), **out)
 
 
-def estimator():
-    from cpfit import CPCompletion
-    rng = np.random.default_rng(71)
-    t, _ = cpfit.gen_low_rank((10, 9, 8), 2, 0.4, rng=cpfit.RngState(72))
-    coords = np.stack(t.coords(), axis=1)
-    perm = rng.permutation(coords.shape[0])
-    X, y = coords[perm], t.values[perm]
-    m = CPCompletion(rank=2, max_iters=6, seed=3, deterministic=True).fit(X, y)
-    Xq = rng.integers(0, 8, (50, 3))
-    out = {"X": X, "y": y, "Xq": Xq, "pred": m.predict(Xq), "score": np.array(m.score(X, y)),
-           "objective": np.array(m.objective_), "n_iter": np.array(m.n_iter_)}
-    for n in range(3):
-        out[f"f{n}"] = m.factors_[n]
-    np.savez_compressed(os.path.join(HERE, "estimator.npz"), **out)
-
-
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -548,7 +531,6 @@ if __name__ == "__main__":
     ingest()
     hypersparse()
     cli()
-    estimator()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
