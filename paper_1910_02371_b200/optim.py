@@ -565,6 +565,11 @@ def _sgd_grads_device(t: SparseTensor, F, rate: float, rng: RngState, dtype,
                 for m in range(t.order)], 0
     if loss is None or loss.device_id == 0:
         phi1 = tttp_affine(sampled, F, 2.0, -2.0, dtype)  # 2(m - t), losses.py:46
+    elif loss.device_id is None:
+        # user-registered loss: model on the device, its host dphi on the values
+        model = tttp_affine(sampled, F, 1.0, 0.0, torch.float64).cpu().numpy()
+        d1 = np.ascontiguousarray(loss.dphi(sampled.values, model), dtype=np.float64)
+        phi1 = torch.from_numpy(d1).to(device=F[0].device, dtype=dtype)
     else:
         from .losses import _count_clamps, device_derivatives
         phi1, _, n = device_derivatives(loss, sampled, F, dtype)
@@ -613,32 +618,12 @@ def _sgd_ls_device(t: SparseTensor, F, cfg: SolverConfig, rng: RngState,
 def sgd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
               cfg: SolverConfig, rng: RngState) -> None:
     """One sampled gradient step on all factors at once (optim.py:300-330)."""
-    if loss.device_id is not None:
-        dtype = None
-        if all(_is_torch(f) and f.dtype == _torch().float32 for f in state.factors):
-            dtype = _torch().float32
-        F = _to_dev_factors(state.factors, dtype)
-        _sgd_ls_device(t, F, cfg, rng, loss)
-        _write_back(state.factors, F)
-        return
-    sampled = t.sample(cfg.sample_rate, rng)
-    factors = state.factors
-    shrink = 2.0 * cfg.step * cfg.reg * cfg.sample_rate
-    if sampled.nnz == 0:
-        for mode in range(t.order):
-            factors[mode] = factors[mode] - shrink * factors[mode]
-        return
-    mask = sampled.observation_mask()
-    model = model_at_observed(mask, factors, threads=cfg.threads)
-    phi1 = sampled.with_values(loss.dphi(sampled.values, model.values))
-    grads = [_as_np(mttkrp(phi1, factors, mode)) for mode in range(t.order)]
-    for mode in range(t.order):
-        cur = _as_np(factors[mode])
-        updated = cur - cfg.step * grads[mode] - shrink * cur
-        if not np.isfinite(np.sum(updated)):
-            raise NumericalError(f"sgd update diverged on mode {mode}; the learning rate is "
-                                 "too high for this sample rate")
-        factors[mode] = _like(factors[mode], updated)
+    dtype = None
+    if all(_is_torch(f) and f.dtype == _torch().float32 for f in state.factors):
+        dtype = _torch().float32
+    F = _to_dev_factors(state.factors, dtype)
+    _sgd_ls_device(t, F, cfg, rng, loss)
+    _write_back(state.factors, F)
 
 
 # ---------------------------------------------------------------------------
