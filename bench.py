@@ -167,6 +167,32 @@ def algorithmic_bytes(order, nnz, rank, dims, vbytes=8, ibytes=4):
     return tttp, mtt, compulsory
 
 
+def compulsory_bytes(order, nnz, rank, dims, vbytes=8, ibytes=4):
+    """SURVEY.md 8(d) compulsory bytes per launch: the nonzero stream plus every
+    factor / output row touched once (what HBM must deliver at least).
+    TTTP: m (N s_i + 2 s_v) + sum_k I_k R s_v; MTTKRP mode n: m (N s_i + s_v)
+    + sum_k I_k R s_v (the output I_n x R included)."""
+    facs = sum(dims) * rank * vbytes
+    tttp = nnz * (order * ibytes + 2 * vbytes) + facs
+    mtt = nnz * (order * ibytes + vbytes) + facs
+    return tttp, mtt
+
+
+def nccl_summary(path, world):
+    """Rank 0's NCCL INIT log (NCCL_DEBUG=INFO): version, communicator sizes,
+    NVLS (NVSwitch multicast / in-switch reduction) availability."""
+    import re
+    try:
+        text = open(path).read()
+    except (OSError, TypeError):
+        return {"log": None}
+    sizes = sorted({int(x) for x in re.findall(r"nRanks (\d+)", text)})
+    ver = re.search(r"NCCL version ([0-9.]+)", text)
+    return {"log": path, "lines": text.count("\n"), "version": ver.group(1) if ver else None,
+            "comm_nranks": sizes, "comm_nranks_ok": world in sizes,
+            "nvls": bool(re.search(r"NVLS multicast support is available|NVLS comm", text))}
+
+
 def run_reference(args):
     """CPU arm: the reference algorithm (oracle C restatement), all host threads."""
     rank = int(os.environ.get("RANK", "0"))
@@ -243,11 +269,20 @@ def cpu_baseline_sample(seconds=12.0):
                       "oracle/cpfit_oracle.c on all host threads"}
 
 
-CPU_ALS_SURVEY_S = 125.0   # reference ALS sweep, cfg 3 full, 8 vCPU (SURVEY.md 6 / BASELINE.md 2)
-CPU_CCD_SURVEY_S = 562.0   # reference CCD++ sweep, same host
+def cpu_info():
+    """Host cores used by the CPU legs and the CPU model (this box)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cores": os.cpu_count() or 1, "model": model}
 
 
-def als_section(world, rank, dev, sweeps=3):
+def als_section(world, rank, dev, sweeps=3, cpu=True):
     """BASELINE cfg 3 (480,189 x 17,770 x 2,182, 100,480,507 Zipf nnz, R=32,
     lambda=1e-5): device-generated seeded instance; ALS sweep time at N GPUs
     (row-sharded with an NCCL all-gather per mode when N > 1; strong scaling),
@@ -310,7 +345,6 @@ def als_section(world, rank, dev, sweeps=3):
         b.record(stream)
         torch.cuda.synchronize()
         out["ccd_sweep_ms"] = a.elapsed_time(b)
-        out["ccd_sweep_cpu_reference_s"] = CPU_CCD_SURVEY_S
         # one Gauss-Newton step from the ALS iterate
         from paper_1910_02371_b200.optim import CompletionState, SolverConfig
         from paper_1910_02371_b200.second_order import gn_step_device
@@ -396,18 +430,41 @@ def als_section(world, rank, dev, sweeps=3):
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         out["ccd_sweep_ms"] = float(ms.item())
         out["ccd_parallelism"] = f"nnz-sharded x{world}, NCCL all-reduce of (num, den)"
-    out["als_sweep_cpu_reference_s"] = CPU_ALS_SURVEY_S
-    out["als_speedup_vs_cpu_reference"] = CPU_ALS_SURVEY_S * 1e3 / out["als_sweep_ms"]
-    out["cpu_reference_note"] = ("reference cpfit (numba + OpenBLAS, 8 vCPU Xeon) measured in "
-                                 "the survey container; see BASELINE.md 2")
+    if cpu and rank == 0 and world == 1:
+        # the reference's CPU algorithm on THIS box's host cores: the oracle's C
+        # restatement (OpenMP over rows as numba's prange) of one full-size ALS
+        # sweep and one CCD++ sweep on the same tensor and init
+        from oracle import oracle as O
+        info = cpu_info()
+        O.set_threads(info["cores"])
+        t0 = time.perf_counter()
+        ot = O.OTensor(shape, t.keys, t.values)
+        for mode in range(3):
+            ot.mode_group(mode)
+        setup = time.perf_counter() - t0
+        host_init = [f.cpu().numpy() for f in init]
+        Fh = [f.copy() for f in host_init]
+        t0 = time.perf_counter()
+        O.als_sweep(ot, Fh, REG)
+        als_s = time.perf_counter() - t0
+        Fh = [f.copy() for f in host_init]
+        t0 = time.perf_counter()
+        O.ccd_sweep(ot, Fh, REG)
+        ccd_s = time.perf_counter() - t0
+        out["cpu_reference"] = {
+            "als_sweep_s": als_s, "ccd_sweep_s": ccd_s, "coords_and_mode_sorts_s": setup,
+            "kind": "port", **info,
+            "sample": "full cfg 3 tensor (100,480,507 nnz, R=32), one ALS sweep and one CCD++ "
+                      "sweep from the bench's init, oracle/cpfit_oracle.c on all host cores"}
+        out["als_speedup_vs_cpu"] = als_s * 1e3 / out["als_sweep_ms"]
+        out["ccd_speedup_vs_cpu"] = ccd_s * 1e3 / out["ccd_sweep_ms"]
+        del ot
     return out
 
 
-CPU_DENSE_EINSUM_S = [1.80, 0.44, 0.47]  # host numpy.einsum per mode, 8 vCPU
-CPU_CFG5_SCALED = {"tttp_s_at_1e7": 3.56, "sgd_step_s_at_1e7": 1.11}  # SURVEY.md 6, f64 numpy
 
 
-def sgd_section(dev, steps=5, world=1):
+def sgd_section(dev, steps=5, world=1, cpu=True):
     """BASELINE cfg 5 on one GPU: order-4 fp32 tensor 1e5^3 x 1e3 with 1e9
     distinct uniform nonzeros (device-generated, values = rank-8 CP model +
     N(0, 0.1) via the library's TTTP), R=64: SGD steps (1% Bernoulli sample,
@@ -480,10 +537,40 @@ def sgd_section(dev, steps=5, world=1):
             "tttp_residual_nnz_per_s": t.nnz / (tttp_ms * 1e-3),
             "tttp_residual_alg_gbs": alg / (tttp_ms * 1e-3) / 1e9,
             "rmse_after": rmse,
-            "cpu_reference_scaled": {"tttp_s": CPU_CFG5_SCALED["tttp_s_at_1e7"] * 100,
-                                     "sgd_step_s": CPU_CFG5_SCALED["sgd_step_s_at_1e7"] * 100,
-                                     "note": "reference f64 numpy path at 1e7 nnz x 100 "
-                                             "(1e9 does not fit the reference host; SURVEY 8d)"}}
+            "cpu_reference": cfg5_cpu_reference(dev) if (cpu and world == 1) else None}
+
+
+def cfg5_cpu_reference(dev, nnz=10_000_000):
+    """cfg 5's CPU reference on this box, at a 1e7-nonzero sample of the cfg 5
+    laws (1e9 order-4 nonzeros do not fit the reference's host path, SURVEY.md
+    8(d)): the oracle's TTTP residual and one SGD step (rate 0.01) in fp64 on
+    all host cores, scaled by nnz to 1e9."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_1910_02371_b200 import synth
+    info = cpu_info()
+    O.set_threads(info["cores"])
+    shape, t, values, F = synth.cfg5_device(nnz=nnz)
+    ot = O.OTensor(shape, t.keys, values.cpu().numpy().astype(np.float64))
+    fs = [f.cpu().numpy().astype(np.float64) for f in F]
+    del t, values, F
+    torch.cuda.empty_cache()
+    t0 = time.perf_counter()
+    ot.coords()
+    setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.tttp(ot.with_values(np.ones(ot.nnz)), fs)
+    tttp_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.sgd_sweep(ot, fs, 1e-4, 1e-3, 0.01, 5, (1, 1))
+    sgd_s = time.perf_counter() - t0
+    scale = 1_000_000_000 / nnz
+    return {"tttp_s_at_sample": tttp_s, "sgd_step_s_at_sample": sgd_s, "coords_s": setup,
+            "tttp_s_scaled_1e9": tttp_s * scale, "sgd_step_s_scaled_1e9": sgd_s * scale,
+            "kind": "port", **info,
+            "sample": f"{nnz} nonzeros with the cfg 5 shape/laws (order 4, R=64), fp64 oracle "
+                      "on all host cores, linear in nnz to 1e9"}
 
 
 def ingest_section(dev, reps=3):
@@ -566,7 +653,24 @@ def pairwise_section(dev, reps=3):
     return out
 
 
-def dense_section(dev, sweeps=2):
+def dense_cpu_reference(X, F):
+    """cfg 4 on the host cores of this box: numpy.einsum('ijk,jr,kr->ir',
+    optimize=True) per mode (the reference has no dense path; SURVEY.md 6 used
+    the same yardstick)."""
+    info = cpu_info()
+    Xh = X.cpu().numpy()
+    A, B, C = (f.cpu().numpy() for f in F)
+    specs = [("ijk,jr,kr->ir", B, C), ("ijk,ir,kr->jr", A, C), ("ijk,ir,jr->kr", A, B)]
+    secs = []
+    for spec, U, V in specs:
+        t0 = time.perf_counter()
+        np.einsum(spec, Xh, U, V, optimize=True)
+        secs.append(time.perf_counter() - t0)
+    return {"numpy_einsum_s_per_mode": secs, "kind": "numpy.einsum (no reference dense path)",
+            **info, "sample": "full 800^3 fp64 tensor, R=64, one call per mode"}
+
+
+def dense_section(dev, sweeps=2, cpu=True):
     """BASELINE cfg 4: dense 800^3 fp64 N(0,1), R=64 factors N(0,1): dense
     MTTKRP per mode and CP-ALS sweep time, against the on-box DGEMM peak."""
     import torch
@@ -598,16 +702,29 @@ def dense_section(dev, sweeps=2):
     del a
     Fs = [f.clone() for f in F]
     sweep_ms = timed(lambda: DN.dense_als_sweep(X, Fs, 1e-5), reps=sweeps)
+    # TF32 tcgen05 variant on the fp32-rounded tensor: HBM-bound (X read once)
+    X32 = X.float()
+    F32 = [f.float() for f in F]
+    tf32_ms = [timed(lambda m=m: DN.dense_mttkrp(X32, F32, m)) for m in range(3)]
+    hbm, _ = peaks()
+    del X32
     return {"workload": "BASELINE cfg 4: dense 800^3 fp64 N(0,1), R=64, lambda=1e-5",
+            "kernels": "dense_dmma_kernel (FP64 DMMA, TMA X tiles, Khatri-Rao tile in smem, "
+                       "split-K with ordered partial sums); dense_tc_kernel (TF32 tcgen05.mma, "
+                       "TMEM accumulator) for fp32",
             "mttkrp_ms": mode_ms,
             "mttkrp_tflops": [flop / (t * 1e-3) / 1e12 for t in mode_ms],
             "dgemm_peak_tflops_measured": peak,
+            "dgemm_peak_what": "cuBLAS DGEMM 8192^3 (torch.matmul float64), measured here as "
+                               "the FP64 denominator only",
             "mttkrp_frac_of_dgemm_peak": [flop / (t * 1e-3) / 1e12 / peak for t in mode_ms],
+            "tf32_mttkrp_ms": tf32_ms,
+            "tf32_hbm_gbs": [n ** 3 * 4 / (t * 1e-3) / 1e9 for t in tf32_ms],
+            "tf32_frac_of_hbm": [n ** 3 * 4 / (t * 1e-3) / 1e9 / hbm for t in tf32_ms],
             "als_sweep_ms": sweep_ms,
-            "als_sweep_flop_model": "2 GEMMs per sweep (X*C shared by modes 0,1; X^T*KR(A,B))",
-            "cpu_numpy_einsum_s_per_mode": CPU_DENSE_EINSUM_S,
-            "cpu_note": "host numpy.einsum(optimize=True), 8 vCPU survey container "
-                        "(the reference has no dense path)"}
+            "als_sweep_flop_model": "2 passes over X per sweep (T = X.C shared by modes 0,1; "
+                                    "mode 2 one Khatri-Rao pass) + Gram / shared-G solve",
+            "cpu_reference": dense_cpu_reference(X, F) if cpu else None}
 
 
 def main():
@@ -617,6 +734,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-ref", action="store_true",
+                    help="skip the on-box CPU reference legs of the cfg 3/4/5 sections")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-als", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
@@ -626,6 +745,16 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
 
     import ctypes
 
@@ -635,9 +764,23 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per "
+                         "GPU (torchrun --nproc-per-node N bench.py --gpus N, or bench.py "
+                         "--gpus N alone, which self-launches)")
     torch.cuda.set_device(local)
+    nccl_log = None
     if world > 1:
+        # NCCL's own init lines (ranks, transports, NVLS) go to a per-rank file;
+        # rank 0 summarises them into the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+        nccl_log = os.environ.setdefault("NCCL_DEBUG_FILE",
+                                         f"/tmp/cpfit_bench_nccl.{os.getpid()}.log")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        warm = torch.ones(1, device=torch.device("cuda", local))
+        dist.all_reduce(warm)  # the communicator is created lazily: force it now
+        torch.cuda.synchronize()
 
     import paper_1910_02371_b200 as cp
     from paper_1910_02371_b200 import _lib, synth
@@ -651,17 +794,16 @@ def main():
     if not args.no_sgd:
         import gc
         try:
-            sgd = sgd_section(dev, world=world)
+            sgd = sgd_section(dev, world=world, cpu=not args.no_cpu_ref)
         except Exception as exc:  # reported, never fatal to the headline line
             sgd = {"error": repr(exc)}
         gc.collect()
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
 
-    shape, keys, values, factors = synth.cfg2(seed=synth.CFG2_SEED + 1000 * rank)
-    if world > 1:
-        # factors are replicated: every rank uses rank 0's draw
-        factors = synth.cfg2(seed=synth.CFG2_SEED, nnz=16)[3]
+    # rank r holds the r-th contiguous nonzero range of one (world x 1e7)-nnz
+    # tensor over the cfg 2 index space; factors replicated
+    shape, keys, values, factors = synth.cfg2_shard(rank, world)
     t = cp.SparseTensor(shape, keys, values, validate=False)
     dev = torch.device("cuda", local)
     dfs = [torch.from_numpy(f).to(dev) for f in factors]
@@ -738,14 +880,14 @@ def main():
     kt = {k: float(np.mean([a.elapsed_time(b) for a, b in v])) for k, v in ev.items()}
     tb, mb, compulsory = algorithmic_bytes(3, t.nnz, R, shape)
     peak, peak_kind = peaks()
-    kernels = {
-        "tttp": {"ms": kt["tttp"], "alg_bytes": tb, "gbs": tb / (kt["tttp"] * 1e-3) / 1e9},
-    }
+    ct, cm = compulsory_bytes(3, t.nnz, R, shape)
+    kernels = {"tttp": {"ms": kt["tttp"], "alg_bytes": tb, "compulsory_bytes": ct}}
     for m in range(3):
-        kernels[f"mttkrp{m}"] = {"ms": kt[f"m{m}"], "alg_bytes": mb[m],
-                                 "gbs": mb[m] / (kt[f"m{m}"] * 1e-3) / 1e9}
+        kernels[f"mttkrp{m}"] = {"ms": kt[f"m{m}"], "alg_bytes": mb[m], "compulsory_bytes": cm}
     for k in kernels.values():
+        k["gbs"] = k["compulsory_bytes"] / (k["ms"] * 1e-3) / 1e9      # HBM-side rate
         k["frac"] = k["gbs"] / peak
+        k["alg_gbs"] = k["alg_bytes"] / (k["ms"] * 1e-3) / 1e9         # incl. L2 gathers
         k["nnz_per_s"] = t.nnz / (k["ms"] * 1e-3)
     # dominant kernel = largest share of the step (MTTKRP runs once per mode)
     share = {"tttp": kernels["tttp"]["ms"],
@@ -756,9 +898,11 @@ def main():
                 "unit": "GB/s", "frac": kernels[dom]["gbs"] / peak, "peak_kind": peak_kind,
                 "step_share": share[dom] / sum(share.values()),
                 "traffic": None,
-                "byte_model": "gather-inclusive algorithmic bytes per launch, SURVEY.md 8(d); "
-                              "the factor-row gathers are served by L1/L2 (see traffic = ncu "
-                              "DRAM bytes per launch, and frac_of_gather_ceiling)"}
+                "byte_model": "compulsory bytes per launch (SURVEY.md 8(d)): the nonzero "
+                              "stream m (N s_i + s_v) plus every factor/output row once, "
+                              "divided by the CUDA-event launch time; the factor-row gathers "
+                              "(gather-inclusive bytes) are L2 traffic, reported in roofline.l2 "
+                              "against the measured L2 read peak"}
     # gather ceiling: the same row gathers with no compute (probe kernel)
     probe = None
     try:
@@ -797,10 +941,47 @@ def main():
         roofline["frac_of_gather_ceiling"] = kernels[dom]["frac_of_gather_ceiling"]
     except Exception as exc:  # the probe is informational
         probe = {"error": str(exc)}
+    # L2 read peak: coalesced passes over an L2-resident buffer (probe kernel)
+    try:
+        l2 = {}
+        lout = torch.empty(num_sms_probe(torch) * 4 * 512, dtype=torch.int32, device=dev)
+        for mb_ in (24, 48, 96):
+            buf = torch.ones(mb_ << 20, dtype=torch.uint8, device=dev)
+
+            def run_l2(reps):
+                _lib.check(L.cpfit_probe_l2_read(ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                                 reps, ctypes.c_void_p(lout.data_ptr()),
+                                                 lout.numel(), sp))
+            run_l2(3)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run_l2(20)
+            b.record(stream)
+            torch.cuda.synchronize()
+            l2[f"{mb_}MB_gbs"] = buf.numel() * 20 / (a.elapsed_time(b) * 1e-3) / 1e9
+            del buf
+        l2_peak = max(l2.values())
+        roofline["l2"] = {"achieved": kernels[dom]["alg_gbs"], "peak": l2_peak, "unit": "GB/s",
+                          "frac_l2": kernels[dom]["alg_gbs"] / l2_peak,
+                          "peak_probe": l2,
+                          "what": "gather-inclusive algorithmic bytes (SURVEY.md 8(d)) per launch "
+                                  "/ launch time, against cpfit_probe_l2_read (max over buffer "
+                                  "sizes of coalesced 16-B ld.global.cg passes over an "
+                                  "L2-resident buffer)"}
+        roofline["frac_l2"] = roofline["l2"]["frac_l2"]
+        for k in kernels.values():
+            k["frac_l2"] = k["alg_gbs"] / l2_peak
+    except Exception as exc:  # informational
+        roofline["l2"] = {"error": repr(exc)}
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            roofline["traffic"] = json.load(open(tf)).get(dom)
+            tr = json.load(open(tf))
+            roofline["traffic"] = tr.get(dom)
+            roofline["traffic_source"] = tr.get("source")
+            if roofline["traffic"]:
+                roofline["achieved_dram"] = roofline["traffic"] / (kernels[dom]["ms"] * 1e-3) / 1e9
+                roofline["frac_dram"] = roofline["achieved_dram"] / peak
         except Exception:
             pass
 
@@ -852,7 +1033,7 @@ def main():
     als = None
     if not args.no_als:
         try:
-            als = als_section(world, rank, dev)
+            als = als_section(world, rank, dev, cpu=not args.no_cpu_ref)
         except Exception as exc:
             als = {"error": repr(exc)}
         torch.cuda.empty_cache()
@@ -872,7 +1053,7 @@ def main():
     dense = None
     if not args.no_dense and world == 1:
         try:
-            dense = dense_section(dev)
+            dense = dense_section(dev, cpu=not args.no_cpu_ref)
         except Exception as exc:
             dense = {"error": repr(exc)}
 
@@ -889,6 +1070,8 @@ def main():
             "als": als, "dense": dense, "sgd": sgd, "ingest": ingest,
             "pairwise_vs_all_at_once": pairwise,
         }
+        if world > 1:
+            line["nccl"] = nccl_summary(nccl_log, world)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample()
         print(json.dumps(line), flush=True)

@@ -42,7 +42,7 @@ SYMBOLS = (
     "cpfit_ccd_gen_update", "cpfit_ccd_gen_model", "cpfit_from_coords",
     "cpfit_tttp_host_async", "cpfit_event_wait", "cpfit_copy_to_host",
     "cpfit_ccsr_spmm", "cpfit_pairwise_tttp", "cpfit_pairwise_fold_sum",
-    "cpfit_dense_mttkrp", "cpfit_dense_xc", "cpfit_dense_gram",
+    "cpfit_dense_mttkrp", "cpfit_dense_xc", "cpfit_dense_gram", "cpfit_probe_l2_read",
 )
 
 _vp = ctypes.c_void_p
@@ -124,6 +124,7 @@ def load(path: str | None = None):
         "cpfit_ccd_fold": [_vp, _int, _PP, _PP, _vp, _vp],
         "cpfit_ccd_finalize": [_i64, _vp, ctypes.c_double, _vp, _vp],
         "cpfit_probe_gather": [_vp, _int, _int, _PP, _i64, _vp, _i64, _vp],
+        "cpfit_probe_l2_read": [_vp, _i64, _int, _vp, _i64, _vp],
         "cpfit_solve_rows": [_int, _int, _i64, _vp, _i64, _vp, ctypes.c_double, _vp,
                              ctypes.POINTER(_i64), _vp],
         "cpfit_dense_reduce": [_int, _i64, _i64, _int, _vp, _vp, _int, _vp, _vp],

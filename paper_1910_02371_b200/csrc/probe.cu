@@ -40,9 +40,46 @@ __global__ void __launch_bounds__(256, 2) probe_gather_kernel(const double2 *__r
   out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// L2 read bandwidth: every thread streams 16-byte vectors of an L2-resident
+// buffer (grid-stride, `reps` passes), folding them into one value per thread
+// so nothing is eliminated.  Coalesced, no reuse inside a CTA: the rate is set
+// by L2 -> SM delivery.
+__global__ void __launch_bounds__(512) probe_l2_kernel(const uint4 *__restrict__ buf, int64_t nvec,
+                                                       int reps, unsigned *out) {
+  unsigned acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < reps; ++r) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < nvec; i += 4 * stride) {
+      uint4 a = __ldcg(buf + i), b = __ldcg(buf + i + stride), c = __ldcg(buf + i + 2 * stride),
+            d = __ldcg(buf + i + 3 * stride);
+      acc ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w ^ d.x ^ d.y ^
+             d.z ^ d.w;
+    }
+    for (; i < nvec; i += stride) {
+      uint4 a = __ldcg(buf + i);
+      acc ^= a.x ^ a.y ^ a.z ^ a.w;
+    }
+  }
+  out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 }  // namespace cpfit
 
 using namespace cpfit;
+
+extern "C" int cpfit_probe_l2_read(const void *buf, int64_t bytes, int reps, void *out,
+                                   int64_t out_len, void *stream) {
+  if (bytes < 16 || reps < 1 || out_len < 512) {
+    set_error("invalid probe_l2_read arguments");
+    return CPFIT_EINVAL;
+  }
+  const int64_t blocks = out_len / 512;
+  probe_l2_kernel<<<(unsigned)blocks, 512, 0, (cudaStream_t)stream>>>(
+      (const uint4 *)buf, bytes / 16, reps, (unsigned *)out);
+  CPFIT_LAUNCH_CHECK("probe_l2_read");
+  return CPFIT_OK;
+}
 
 extern "C" int cpfit_probe_gather(const void *table, int row_bytes, int nrows_per,
                                   const int32_t *const *idx, int64_t n, double *out,

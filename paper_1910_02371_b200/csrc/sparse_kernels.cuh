@@ -32,6 +32,9 @@
 #ifndef CPFIT_MTTKRP_MINB_F32
 #define CPFIT_MTTKRP_MINB_F32 3  // fp32 (cfg 5 SGD samples: 4 cost ~1 ms per step)
 #endif
+#ifndef CPFIT_TTTP_U0
+#define CPFIT_TTTP_U0 4  // TTTP sub-iterations in flight when the mode-0 row is hoisted
+#endif
 #ifndef CPFIT_MTTKRP_U
 #define CPFIT_MTTKRP_U 4  // sub-iterations of gathers in flight per MTTKRP round
 #endif
@@ -64,7 +67,9 @@ struct TttpParams {
 // between).  `fq[n]` is the lane's base pointer (factor n + q*VEC), so a row
 // address is one 32-bit multiply + one wide add; column offsets are
 // immediates.  FULL: the tiling covers the rank exactly (no column predicate).
-template <typename T, int VEC, int LPE, int KV, int NPM, int U, bool FULL>
+// N0 = first mode gathered (1: the mode-0 row is uniform over the batch and
+// already in registers, see tttp_kernel).
+template <typename T, int VEC, int LPE, int KV, int NPM, int U, bool FULL, int N0 = 0>
 __device__ __forceinline__ void gather_rows(const T *const (&fq)[NPM],
                                             const int32_t (&my_idx)[NPM], int np,
                                             unsigned rank, int s0, int g, int q,
@@ -74,7 +79,7 @@ __device__ __forceinline__ void gather_rows(const T *const (&fq)[NPM],
   for (int u = 0; u < U; ++u) {
     const int j = (s0 + u) * G + g;
 #pragma unroll
-    for (int n = 0; n < NPM; ++n) {
+    for (int n = N0; n < NPM; ++n) {
       if (n >= np) break;
       const unsigned row = (unsigned)__shfl_sync(0xffffffffu, my_idx[n], j);
       const T *frow = reinterpret_cast<const T *>(reinterpret_cast<const char *>(fq[n]) +
@@ -173,23 +178,67 @@ __global__ void __launch_bounds__(256, CPFIT_TTTP_MINB) tttp_kernel(const TttpPa
     const T my_val = out_ok ? __ldg(p.vals + eo) : T(0);
     T part[LPE];
     if constexpr (NP > 0) {
+      // canonical (key-sorted) order: the mode-0 index is constant over runs of
+      // nnz / I_0 entries (cfg 2: ~1000, cfg 5: ~10^4), so most batches share
+      // one mode-0 row.  Then it is gathered once per batch into registers and
+      // only the other NP-1 rows per nonzero (same products, same order).
+      const int32_t i0 = __shfl_sync(0xffffffffu, my_idx[0], 0);
+      const bool uni0 = NP > 1 && __all_sync(0xffffffffu, my_idx[0] == i0);
+      if (uni0) {
+        T r0[KV][VEC];
+        {
+          const T *frow = reinterpret_cast<const T *>(
+              reinterpret_cast<const char *>(fq[0]) +
+              (unsigned long long)(unsigned)i0 * (rank * (unsigned)sizeof(T)));
 #pragma unroll
-      for (int s0 = 0; s0 < LPE; s0 += U) {
-        T x[U][NPM][KV][VEC];
-        gather_rows<T, VEC, LPE, KV, NPM, U, FULL>(fq, my_idx, np, rank, s0, g, q, x);
+          for (int k = 0; k < KV; ++k) {
+            if (FULL || (unsigned)((k * LPE + q) * VEC) < rank) {
+              load_vec<T, VEC>(frow + k * LPE * VEC, r0[k]);
+            } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          T acc = T(0);
-#pragma unroll
-          for (int k = 0; k < KV; ++k)
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) {
-              T prod = x[u][0][k][v];
-#pragma unroll
-              for (int n = 1; n < NPM; ++n) prod = prod * x[u][n][k][v];
-              acc += prod;
+              for (int v = 0; v < VEC; ++v) r0[k][v] = T(0);
             }
-          part[s0 + u] = acc;
+          }
+        }
+        constexpr int U0 = U * CPFIT_TTTP_U0 / 4 <= LPE ? U * CPFIT_TTTP_U0 / 4 : LPE;
+#pragma unroll
+        for (int s0 = 0; s0 < LPE; s0 += U0) {
+          T x[U0][NPM][KV][VEC];
+          gather_rows<T, VEC, LPE, KV, NPM, U0, FULL, 1>(fq, my_idx, np, rank, s0, g, q, x);
+#pragma unroll
+          for (int u = 0; u < U0; ++u) {
+            T acc = T(0);
+#pragma unroll
+            for (int k = 0; k < KV; ++k)
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) {
+                T prod = r0[k][v];
+#pragma unroll
+                for (int n = 1; n < NPM; ++n) prod = prod * x[u][n][k][v];
+                acc += prod;
+              }
+            part[s0 + u] = acc;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int s0 = 0; s0 < LPE; s0 += U) {
+          T x[U][NPM][KV][VEC];
+          gather_rows<T, VEC, LPE, KV, NPM, U, FULL>(fq, my_idx, np, rank, s0, g, q, x);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            T acc = T(0);
+#pragma unroll
+            for (int k = 0; k < KV; ++k)
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) {
+                T prod = x[u][0][k][v];
+#pragma unroll
+                for (int n = 1; n < NPM; ++n) prod = prod * x[u][n][k][v];
+                acc += prod;
+              }
+            part[s0 + u] = acc;
+          }
         }
       }
     } else {

@@ -86,6 +86,27 @@ def cfg2(seed: int = CFG2_SEED, nnz: int = 10_000_000, rank: int = 16):
     return shape, keys, values, factors
 
 
+def cfg2_shard(rank: int, world: int, seed: int = CFG2_SEED, nnz: int = 10_000_000,
+               R: int = 16):
+    """Weak-scaling shard ``rank`` of a (world x nnz)-nonzero tensor over the
+    cfg 2 index space: the shard holds nnz distinct uniform keys of the
+    rank's contiguous slice of [0, 10^12), so the union over ranks is one
+    sorted tensor partitioned into contiguous nonzero ranges (SURVEY.md 8(e)
+    nnz sharding).  Factors are replicated (one draw for every rank).
+    world == 1 is exactly ``cfg2``."""
+    if world == 1:
+        return cfg2(seed, nnz, R)
+    space = 10 ** 12
+    lo, hi = space * rank // world, space * (rank + 1) // world
+    rng = np.random.default_rng([seed, rank, world])
+    keys = np.uint64(lo) + distinct_uniform_keys(rng, hi - lo, nnz)
+    values = rng.standard_normal(keys.size)
+    frng = np.random.default_rng([seed, 99])
+    shape = (10_000, 10_000, 10_000)
+    factors = [frng.standard_normal((d, R)) * np.sqrt(1.0 / R) for d in shape]
+    return shape, keys, values, factors
+
+
 def zipf_indices(rng, dim: int, size: int, alpha: float = 1.0) -> np.ndarray:
     """Bounded Zipf(alpha) over 0..dim-1 by inverse CDF on weights 1/k^alpha."""
     w = 1.0 / np.arange(1, dim + 1, dtype=np.float64) ** alpha
