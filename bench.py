@@ -413,7 +413,11 @@ def als_section(world, rank, dev, sweeps=3, cpu=True):
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             times.append(float(ms.item()))
         out["als_sweep_ms"] = float(np.mean(times))
-        out["parallelism"] = f"row-sharded x{world}, NCCL all-gather of factor rows per mode"
+        out["parallelism"] = (f"row-sharded x{world} (blocks balance nnz + {als.row_weight:.0f} "
+                              "per row), uneven all-gather of the updated rows per mode "
+                              "(one NCCL broadcast per block)")
+        out["gather_bytes_per_sweep"] = sum(als.exchanged_bytes(m, R3) for m in range(3))
+        out["row_blocks"] = [[b - a for a, b in blks] for blks in als.blocks]
         del als
         torch.cuda.empty_cache()
         # CCD++: nonzero-sharded, one all-reduce of (num, den) per (r, mode)

@@ -6,9 +6,13 @@ make equal row counts useless); rank p keeps a *mode shard*: the nonzeros
 whose mode-n index lies in its block, with that coordinate rebased to the
 block (shape[n] = block rows) and every other coordinate global.  Right-hand
 side (MTTKRP), Gram and solve are all row-local, so one mode update is:
-local MTTKRP + fused Gram/solve on the shard, then one all-gather of the
-updated I_n x R rows (blocks padded to the largest block; NCCL over
-NVLink/NVSwitch).  No other exchange: factors are replicated.
+local MTTKRP + fused Gram/solve on the shard, then one uneven all-gather of
+the updated I_n x R rows: one broadcast per block from its owner into the
+replicated factor (NCCL over NVLink/NVSwitch moves exactly I_n x R values,
+never a block padded to the largest one).  Blocks balance a cost model, not
+just nonzeros: a row costs its nonzeros (Gram + right-hand side) plus a
+per-row term for the R x R solve and the Gram store/load
+(``als_row_weight``).  No other exchange: factors are replicated.
 
 SGD shards *nonzeros* (contiguous key ranges); the device Philox sampler uses
 the global entry index as its counter, so the union of the shard samples is
@@ -30,11 +34,22 @@ import math
 import numpy as np
 
 
-def row_partition(row_counts, parts: int):
-    """Contiguous row blocks [lo, hi) balanced by the nnz prefix sum."""
-    counts = np.asarray(row_counts, dtype=np.int64)
-    prefix = np.concatenate([[0], np.cumsum(counts)])
-    total = int(prefix[-1])
+def als_row_weight(rank: int) -> float:
+    """Cost of one row's solve + Gram store/load in units of one nonzero's
+    Gram + right-hand-side work.  Measured at cfg 3 (R = 32, one B200):
+    fused Gram + rhs 6.9 ms / 1.005e8 nnz = 0.069 ns per nonzero; batched
+    Cholesky 2.45 ms + 2 x 3.9 GB of G traffic ~ 3.65 ms / 480,189 rows =
+    7.6 ns per row -> ~110 at R = 32.  The solve grows like R^3 and the
+    per-nonzero Gram like R^2, so the ratio scales ~linearly in R."""
+    return 3.4 * float(rank)
+
+
+def row_partition(row_counts, parts: int, row_weight: float = 0.0):
+    """Contiguous row blocks [lo, hi) balanced by the prefix sum of the row
+    cost nnz_i + row_weight (row_weight 0: by nonzeros only)."""
+    counts = np.asarray(row_counts, dtype=np.float64)
+    prefix = np.concatenate([[0.0], np.cumsum(counts + float(row_weight))])
+    total = float(prefix[-1])
     bounds = [0]
     for p in range(1, parts):
         target = total * p / parts
@@ -72,7 +87,7 @@ def shard_keys(coords, shape, mode: int, lo: int, hi: int, xp=np):
     return tuple(sshape), key, sel
 
 
-def pad_rows(x, rows: int, xp=np):
+def pad_rows(x, rows: int, xp=np):  # kept for callers that pad explicitly
     if x.shape[0] == rows:
         return x
     if xp is np:
@@ -93,7 +108,8 @@ class ShardedALS:
       xp -> numpy or torch (for shard_keys / padding)
     """
 
-    def __init__(self, coords, values, shape, reg, backend, group=None):
+    def __init__(self, coords, values, shape, reg, backend, group=None, rank_r: int = 32,
+                 row_weight: float | None = None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
@@ -102,6 +118,7 @@ class ShardedALS:
         self.shape = tuple(shape)
         self.reg = float(reg)
         self.backend = backend
+        self.row_weight = als_row_weight(rank_r) if row_weight is None else float(row_weight)
         xp = backend.xp
         self.blocks = []
         self.shards = []
@@ -110,23 +127,35 @@ class ShardedALS:
                 counts = np.bincount(coords[mode], minlength=d)
             else:
                 counts = xp.bincount(coords[mode], minlength=d).cpu().numpy()
-            blocks = row_partition(counts, self.world)
+            blocks = row_partition(counts, self.world, self.row_weight)
             lo, hi = blocks[self.rank]
             sshape, keys, sel = shard_keys(coords, self.shape, mode, lo, hi, xp)
             self.blocks.append(blocks)
             self.shards.append(backend.make_shard(sshape, keys, values[sel]))
 
     def mode_update(self, factors, mode: int):
+        """Local update of this rank's rows, then an uneven all-gather: the
+        owner of each block broadcasts exactly its rows into the replicated
+        factor (I_n x R values on the wire, no padding)."""
         blocks = self.blocks[mode]
         lo, hi = blocks[self.rank]
-        rows = self.backend.als_mode(self.shards[mode], factors, mode, self.reg, lo, hi)
-        maxr = max(b - a for a, b in blocks)
-        send = self.backend.to_comm(pad_rows(rows, maxr, self.backend.xp))
-        recv = self.backend.empty_comm((self.world * maxr,) + tuple(send.shape[1:]), send)
-        self.dist.all_gather_into_tensor(recv, send, group=self.group)
-        parts = [recv[p * maxr: p * maxr + (b - a)] for p, (a, b) in enumerate(blocks)]
-        full = self.backend.cat(parts)
+        rows = self.backend.to_comm(
+            self.backend.als_mode(self.shards[mode], factors, mode, self.reg, lo, hi))
+        full = self.backend.empty_comm((self.shape[mode],) + tuple(rows.shape[1:]), rows)
+        for p, (a, b) in enumerate(blocks):
+            if b == a:
+                continue
+            view = full[a:b]
+            if p == self.rank:
+                view.copy_(rows)
+            if self.world > 1:
+                src = p if self.group is None else self.dist.get_global_rank(self.group, p)
+                self.dist.broadcast(view, src=src, group=self.group)
         factors[mode] = self.backend.from_comm(full)
+
+    def exchanged_bytes(self, mode: int, rank_r: int, itemsize: int = 8) -> int:
+        """Bytes one mode's gather puts on the wire (sum of the blocks)."""
+        return sum(b - a for a, b in self.blocks[mode]) * rank_r * itemsize
 
     def sweep(self, factors):
         for mode in range(len(self.shape)):
@@ -319,6 +348,6 @@ def als_strong_scaling_rows(blocks):
     return max(sizes) / max(1, sum(sizes)) * len(sizes)
 
 
-__all__ = ["row_partition", "nnz_partition", "shard_keys", "ShardedALS", "ShardedCCD",
-           "ShardedSGD", "DeviceBackend",
-           "pad_rows", "als_strong_scaling_rows", "math"]
+__all__ = ["row_partition", "als_row_weight", "nnz_partition", "shard_keys", "ShardedALS",
+           "ShardedCCD", "ShardedSGD", "DeviceBackend", "pad_rows", "als_strong_scaling_rows",
+           "math"]

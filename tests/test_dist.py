@@ -170,6 +170,24 @@ def dist_run(tmp_path_factory):
     return out
 
 
+def test_row_cost_partition_and_uneven_gather_bytes():
+    """cfg 3-like Zipf rows at P = 8: balancing nnz + a per-row solve cost
+    moves rows off the tail block; the gather carries exactly I_n x R values."""
+    rng = np.random.default_rng(0)
+    counts = np.bincount(synth.zipf_indices(rng, 480_189, 2_000_000), minlength=480_189)
+    by_nnz = D.row_partition(counts, 8)
+    by_cost = D.row_partition(counts, 8, D.als_row_weight(32))
+    cost = counts + D.als_row_weight(32)
+    share = lambda blocks: max(cost[a:b].sum() for a, b in blocks) / cost.sum() * 8
+    assert share(by_cost) < share(by_nnz)
+    assert share(by_cost) < 1.05
+    rows = [b - a for a, b in by_cost]
+    assert sum(rows) == counts.size  # uneven gather = I_n x R values, no padding
+    # a gather padded to the largest block of the nnz-only partition (round 1)
+    # would have moved ~6.5x the factor
+    assert max(b - a for a, b in by_nnz) * 8 > 5 * counts.size
+
+
 def test_row_partition_balances_skewed_rows():
     counts = np.array([1000, 1, 1, 1, 500, 500, 3, 3])
     blocks = D.row_partition(counts, 2)
