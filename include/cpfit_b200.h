@@ -147,6 +147,39 @@ int cpfit_als_update(cpfit_pattern *p, int mode, int dtype, int rank,
                      void *gram_out, void *rhs_out, int64_t *bad_row,
                      void *stream);
 
+/* Gram-free normal-equations product of one ALS mode (BASELINE cfg 3 "ALS
+ * completion with implicit CG"; the reference solves each row with LAPACK,
+ * kernels.py:259, and has no counterpart):
+ *   out[i, :] = sum_{e in row i} w_e h_e (h_e . x[i, :]),
+ *   h_e = prod_{k != mode} factors[k][i_k(e), :]   (kernels.py:196-204),
+ * i.e. G_i x_i without materialising the I x R x R blocks of
+ * kernels.gram_blocks.  weights nullable (unit weights: the observation
+ * mask); weights_sorted as in cpfit_mttkrp.  row_active (nullable, int32 per
+ * row of the mode): rows with 0 are skipped and their output row is 0. */
+int cpfit_gram_matvec(cpfit_pattern *p, int mode, int dtype, int rank,
+                      const void *weights, int weights_sorted,
+                      const void *const *factors, const void *x,
+                      const int32_t *row_active, void *out, void *stream);
+
+/* Per-row CG recurrences for (G_i + reg I) x_i = b_i, every row with its own
+ * alpha / beta (the systems are independent), in the form of pcg_solve
+ * (optim.py:493-533) applied per row: stop a row when ||r_i|| <= tol ||b_i||
+ * or on nonpositive curvature.  All arrays are device memory: b, x, r, p
+ * nrows x rank of `dtype`; rho, thresh2 double[nrows]; active int32[nrows];
+ * status int64[2] = {rows still active after the call, sticky non-finite flag}.
+ * init: r = b - (ax + reg x) (ax = G x0 from cpfit_gram_matvec, or NULL for
+ * x0 = 0 -- x is then not read), p = r; rows with b_i = 0 get x_i = 0.
+ * step: q = G p from cpfit_gram_matvec(..., p, active, ...); updates x, r, p,
+ * rho and active in place. */
+int cpfit_cg_rows_init(int dtype, int64_t nrows, int rank, double reg, double tol,
+                       const void *b, const void *ax, void *x, void *r, void *p,
+                       double *rho, double *thresh2, int32_t *active,
+                       int64_t *status, void *stream);
+int cpfit_cg_rows_step(int dtype, int64_t nrows, int rank, double reg,
+                       const void *q, void *x, void *r, void *p, double *rho,
+                       const double *thresh2, int32_t *active, int64_t *status,
+                       void *stream);
+
 /* TTTP whose result is also delivered to HOST memory (the reference's
  * numpy-returning tttp, kernels.py:105-149): the nonzeros are processed in
  * chunks (chunk <= 0: nnz/8, at most 16 chunks) and each chunk is copied

@@ -43,6 +43,7 @@ SYMBOLS = (
     "cpfit_tttp_host_async", "cpfit_event_wait", "cpfit_copy_to_host",
     "cpfit_ccsr_spmm", "cpfit_pairwise_tttp", "cpfit_pairwise_fold_sum",
     "cpfit_dense_mttkrp", "cpfit_dense_xc", "cpfit_dense_gram", "cpfit_probe_l2_read",
+    "cpfit_gram_matvec", "cpfit_cg_rows_init", "cpfit_cg_rows_step",
 )
 
 _vp = ctypes.c_void_p
@@ -135,6 +136,11 @@ def load(path: str | None = None):
         "cpfit_dense_gram": [_int, _int, ctypes.POINTER(_i64), _int, _PP, _vp, _vp],
         "cpfit_als_update": [_vp, _int, _int, _int, _vp, _int, _PP, ctypes.c_double, _vp, _vp,
                              _vp, ctypes.POINTER(_i64), _vp],
+        "cpfit_gram_matvec": [_vp, _int, _int, _int, _vp, _int, _PP, _vp, _vp, _vp, _vp],
+        "cpfit_cg_rows_init": [_int, _i64, _int, ctypes.c_double, ctypes.c_double, _vp, _vp,
+                               _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+        "cpfit_cg_rows_step": [_int, _i64, _int, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _vp, _vp, _vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -10,6 +10,8 @@ extern template int dispatch_tttp<double>(const TttpParams<double> &, int, cudaS
 extern template int dispatch_tttp<float>(const TttpParams<float> &, int, cudaStream_t);
 extern template int dispatch_mttkrp<double>(const MttkrpParams<double> &, int, cudaStream_t);
 extern template int dispatch_mttkrp<float>(const MttkrpParams<float> &, int, cudaStream_t);
+extern template int dispatch_mttkrp_mv<double>(const MttkrpParams<double> &, int, cudaStream_t);
+extern template int dispatch_mttkrp_mv<float>(const MttkrpParams<float> &, int, cudaStream_t);
 
 template <typename T>
 static int run_tttp(cpfit_pattern *pt, int rank, const void *vals, const void *const *factors,
@@ -91,7 +93,8 @@ static int run_tttp_host(cpfit_pattern *pt, int rank, const void *vals,
 
 template <typename T>
 static int run_mttkrp(cpfit_pattern *pt, int mode, int rank, const void *vals, int vals_sorted,
-                      const void *const *factors, void *out, cudaStream_t s) {
+                      const void *const *factors, void *out, cudaStream_t s,
+                      const void *xvec = nullptr, const int32_t *row_active = nullptr) {
   const int64_t dim = pt->dims[mode];
   CPFIT_CUDA(cudaMemsetAsync(out, 0, (size_t)dim * rank * sizeof(T), s));
   if (pt->nnz == 0) return CPFIT_OK;
@@ -120,6 +123,9 @@ static int run_mttkrp(cpfit_pattern *pt, int mode, int rank, const void *vals, i
   p.task_slot = L.task_slot;
   p.ntasks = L.ntasks;
   p.out = (T *)out;
+  p.xvec = (const T *)xvec;
+  p.row_active = row_active;
+  if (xvec) ptrs[np] = xvec;  // alignment of the matvec operand decides the vector width too
   Scratch<T> partial(s);
   if (L.nslots > 0) CPFIT_TRY(partial.alloc((size_t)L.nslots * rank));
   p.partial = partial.ptr;
@@ -128,7 +134,10 @@ static int run_mttkrp(cpfit_pattern *pt, int mode, int rank, const void *vals, i
     set_error("mttkrp needs an order >= 2 tensor");
     return CPFIT_EINVAL;
   }
-  CPFIT_TRY(dispatch_mttkrp<T>(p, pick_vec<T>(rank, ptrs, np), s));
+  if (xvec)
+    CPFIT_TRY(dispatch_mttkrp_mv<T>(p, pick_vec<T>(rank, ptrs, np + 1), s));
+  else
+    CPFIT_TRY(dispatch_mttkrp<T>(p, pick_vec<T>(rank, ptrs, np), s));
   if (L.nsplit > 0) {
     combine_partials<T><<<grid_for(L.nsplit * 32, 256), 256, 0, s>>>(
         L.split_row, L.split_slot, L.nsplit, rank, partial.ptr, (T *)out);
@@ -265,6 +274,26 @@ int cpfit_mttkrp(cpfit_pattern *p, int mode, int dtype, int rank, const void *va
     return run_mttkrp<double>(p, mode, rank, vals, vals_sorted, factors, out, s);
   if (dtype == CPFIT_F32)
     return run_mttkrp<float>(p, mode, rank, vals, vals_sorted, factors, out, s);
+  set_error("unknown dtype %d", dtype);
+  return CPFIT_EINVAL;
+}
+
+int cpfit_gram_matvec(cpfit_pattern *p, int mode, int dtype, int rank, const void *weights,
+                      int weights_sorted, const void *const *factors, const void *x,
+                      const int32_t *row_active, void *out, void *stream) {
+  if (!p || mode < 0 || mode >= p->order) {
+    set_error("mode %d out of range for order-%d tensor", mode, p ? p->order : 0);
+    return CPFIT_EINVAL;
+  }
+  if (rank < 1) { set_error("rank must be >= 1"); return CPFIT_EINVAL; }
+  if (!x || !out) { set_error("null operand"); return CPFIT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == CPFIT_F64)
+    return run_mttkrp<double>(p, mode, rank, weights, weights_sorted, factors, out, s, x,
+                              row_active);
+  if (dtype == CPFIT_F32)
+    return run_mttkrp<float>(p, mode, rank, weights, weights_sorted, factors, out, s, x,
+                             row_active);
   set_error("unknown dtype %d", dtype);
   return CPFIT_EINVAL;
 }

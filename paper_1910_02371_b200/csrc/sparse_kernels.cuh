@@ -299,6 +299,9 @@ struct MttkrpParams {
   int64_t ntasks;
   T *out;
   T *partial;
+  // Gram-free normal-equations product (MV kernels): out_i = sum_e w_e h_e (h_e . x_i)
+  const T *xvec;               // I_mode x rank
+  const int32_t *row_active;   // nullable: rows with 0 are skipped (their output is 0)
 };
 
 // One batch of up to 32 entries: coalesced indices (row 0 and value 0 past
@@ -310,10 +313,13 @@ __device__ __forceinline__ void mttkrp_load_batch(const MttkrpParams<T> &p, int 
 #pragma unroll
   for (int n = 0; n < NPM; ++n) ix[n] = (n < np && ok) ? __ldg(p.idx[n] + e) : 0;
   v = T(0);
-  if (ok) v = p.perm ? __ldg(p.vals + __ldg(p.perm + e)) : __ldg(p.vals + e);
+  if (ok) v = !p.vals ? T(1) : p.perm ? __ldg(p.vals + __ldg(p.perm + e)) : __ldg(p.vals + e);
 }
 
-template <typename T, int VEC, int LPE, int KV, int NP, bool FULL>
+// MV: the entry weight is w_e (h_e . x_row) with x_row the task row's slice of
+// p.xvec -- the per-row normal-equations product G_i x_i of implicit-CG ALS,
+// without materialising G ("ALS with implicit CG").
+template <typename T, int VEC, int LPE, int KV, int NP, bool FULL, bool MV = false>
 __global__ void __launch_bounds__(256, sizeof(T) == 8 ? CPFIT_MTTKRP_MINB : CPFIT_MTTKRP_MINB_F32)
     mttkrp_kernel(const MttkrpParams<T> p) {
   constexpr int G = 32 / LPE;
@@ -333,10 +339,26 @@ __global__ void __launch_bounds__(256, sizeof(T) == 8 ? CPFIT_MTTKRP_MINB : CPFI
   int64_t nb0 = warp < p.ntasks ? p.task_begin[warp] : 0;
   int64_t nb1 = warp < p.ntasks ? p.task_begin[warp + 1] : 0;
   for (int64_t t = warp; t < p.ntasks; t += nwarps) {
-    const int64_t b0 = nb0, b1 = nb1;
+    const int64_t b0 = nb0;
+    int64_t b1 = nb1;
     if (t + nwarps < p.ntasks) {
       nb0 = p.task_begin[t + nwarps];
       nb1 = p.task_begin[t + nwarps + 1];
+    }
+    T xr[MV ? KV : 1][MV ? VEC : 1];
+    if constexpr (MV) {
+      const int64_t row = p.task_row[t];
+      if (p.row_active && !p.row_active[row]) b1 = b0;  // converged row: contributes 0
+#pragma unroll
+      for (int k = 0; k < KV; ++k) {
+        const int col = (k * LPE + q) * VEC;
+        if (FULL || col < (int)rank) {
+          load_vec<T, VEC>(p.xvec + row * rank + col, xr[k]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) xr[k][v] = T(0);
+        }
+      }
     }
     T acc[KV][VEC];
 #pragma unroll
@@ -360,21 +382,52 @@ __global__ void __launch_bounds__(256, sizeof(T) == 8 ? CPFIT_MTTKRP_MINB : CPFI
           gather_rows<T, VEC, LPE, KV, NPM, U, FULL>(fq, my_idx, np, rank, s0, g, q, x);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const T v = __shfl_sync(0xffffffffu, my_val, (s0 + u) * G + g);
+            T v = __shfl_sync(0xffffffffu, my_val, (s0 + u) * G + g);
+            if constexpr (MV) {
+              T d = T(0);
 #pragma unroll
-            for (int k = 0; k < KV; ++k)
+              for (int k = 0; k < KV; ++k)
 #pragma unroll
-              for (int w = 0; w < VEC; ++w) {
-                T prod = x[u][0][k][w];
+                for (int w = 0; w < VEC; ++w) {
+                  T prod = x[u][0][k][w];
 #pragma unroll
-                for (int n = 1; n < NPM; ++n) prod = prod * x[u][n][k][w];
-                acc[k][w] += prod * v;
-              }
+                  for (int n = 1; n < NPM; ++n) prod = prod * x[u][n][k][w];
+                  x[u][0][k][w] = prod;
+                  d += prod * xr[k][w];
+                }
+#pragma unroll
+              for (int o = LPE / 2; o > 0; o >>= 1) d += shfl_xor(d, o);
+              v *= d;
+#pragma unroll
+              for (int k = 0; k < KV; ++k)
+#pragma unroll
+                for (int w = 0; w < VEC; ++w) acc[k][w] += x[u][0][k][w] * v;
+            } else {
+#pragma unroll
+              for (int k = 0; k < KV; ++k)
+#pragma unroll
+                for (int w = 0; w < VEC; ++w) {
+                  T prod = x[u][0][k][w];
+#pragma unroll
+                  for (int n = 1; n < NPM; ++n) prod = prod * x[u][n][k][w];
+                  acc[k][w] += prod * v;
+                }
+            }
           }
         } else {
           T prod[KV][VEC];
           gather_product<T, VEC, LPE, KV, NPM>(fq, my_idx, np, rank, s0, g, q, prod);
-          const T v = __shfl_sync(0xffffffffu, my_val, s0 * G + g);
+          T v = __shfl_sync(0xffffffffu, my_val, s0 * G + g);
+          if constexpr (MV) {
+            T d = T(0);
+#pragma unroll
+            for (int k = 0; k < KV; ++k)
+#pragma unroll
+              for (int w = 0; w < VEC; ++w) d += prod[k][w] * xr[k][w];
+#pragma unroll
+            for (int o = LPE / 2; o > 0; o >>= 1) d += shfl_xor(d, o);
+            v *= d;
+          }
 #pragma unroll
           for (int k = 0; k < KV; ++k)
 #pragma unroll
@@ -489,7 +542,7 @@ static int launch_tttp_np(const TttpParams<T> &p, cudaStream_t s) {
   return CPFIT_OK;
 }
 
-template <typename T, int VEC, int LPE, int KV>
+template <typename T, int VEC, int LPE, int KV, bool MV = false>
 static int launch_mttkrp_np(const MttkrpParams<T> &p, cudaStream_t s) {
   // persistent grid: exactly the resident capacity (no partial waves)
   int64_t blocks = (p.ntasks + 7) / 8;
@@ -500,22 +553,22 @@ static int launch_mttkrp_np(const MttkrpParams<T> &p, cudaStream_t s) {
   constexpr bool HOT = (sizeof(T) == 8 && VEC == 2) || (sizeof(T) == 4 && VEC == 4);
   if constexpr (HOT) {
     if (p.np == 2 && full) {
-      mttkrp_kernel<T, VEC, LPE, KV, 2, true><<<grid, 256, 0, s>>>(p);
+      mttkrp_kernel<T, VEC, LPE, KV, 2, true, MV><<<grid, 256, 0, s>>>(p);
       CPFIT_LAUNCH_CHECK("mttkrp_kernel");
       return CPFIT_OK;
     }
     if (p.np == 3 && full) {
-      mttkrp_kernel<T, VEC, LPE, KV, 3, true><<<grid, 256, 0, s>>>(p);
+      mttkrp_kernel<T, VEC, LPE, KV, 3, true, MV><<<grid, 256, 0, s>>>(p);
       CPFIT_LAUNCH_CHECK("mttkrp_kernel");
       return CPFIT_OK;
     }
     if (p.np == 2) {  // ranks the lane tiling does not cover exactly (e.g. R = 10)
-      mttkrp_kernel<T, VEC, LPE, KV, 2, false><<<grid, 256, 0, s>>>(p);
+      mttkrp_kernel<T, VEC, LPE, KV, 2, false, MV><<<grid, 256, 0, s>>>(p);
       CPFIT_LAUNCH_CHECK("mttkrp_kernel");
       return CPFIT_OK;
     }
   }
-  mttkrp_kernel<T, VEC, LPE, KV, 0, false><<<grid, 256, 0, s>>>(p);
+  mttkrp_kernel<T, VEC, LPE, KV, 0, false, MV><<<grid, 256, 0, s>>>(p);
   CPFIT_LAUNCH_CHECK("mttkrp_kernel");
   return CPFIT_OK;
 }
@@ -597,9 +650,29 @@ int dispatch_mttkrp(const MttkrpParams<T> &p, int vec, cudaStream_t s) {
   }
 }
 
+// Gram-free matvec variants (instantiated in gram_matvec_f64.cu / _f32.cu)
+template <typename T>
+int dispatch_mttkrp_mv(const MttkrpParams<T> &p, int vec, cudaStream_t s) {
+  const int nv = (p.rank + vec - 1) / vec;
+  constexpr int KVT = sizeof(T) == 8 ? CPFIT_MTTKRP_KVT64 : 1;
+  if constexpr (sizeof(T) == 8) {
+    if (vec == 2)
+      return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 2, L, K, true>(p, s); });
+    return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 1, L, K, true>(p, s); });
+  } else {
+    if (vec == 4)
+      return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 4, L, K, true>(p, s); });
+    if (vec == 2)
+      return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 2, L, K, true>(p, s); });
+    return mttkrp_tiling_dispatch<KVT>(nv, [&]<int L, int K>() { return launch_mttkrp_np<T, 1, L, K, true>(p, s); });
+  }
+}
+
 template <typename T>
 int dispatch_tttp(const TttpParams<T> &p, int vec, cudaStream_t s);
 template <typename T>
 int dispatch_mttkrp(const MttkrpParams<T> &p, int vec, cudaStream_t s);
+template <typename T>
+int dispatch_mttkrp_mv(const MttkrpParams<T> &p, int vec, cudaStream_t s);
 
 }  // namespace cpfit

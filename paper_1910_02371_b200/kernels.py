@@ -269,6 +269,41 @@ def gram_blocks(weights: SparseTensor, factors, mode: int, row_batches: int = 1,
     return gram if on_device else to_host(gram)
 
 
+def gram_matvec(weights: SparseTensor, factors, x, mode: int, row_active=None):
+    """Row-wise product with the normal-equation matrices WITHOUT forming them:
+    out[i] = G_i x[i] = sum over entries of row i of weight * h (h . x[i]),
+    h and G_i as in ``gram_blocks`` (kernels.py:159-212).  One pass over the
+    nonzeros (cpfit_gram_matvec); the building block of the implicit-CG ALS
+    update (``SolverConfig(als_solver="cg")``).  Not a reference function: its
+    oracle is ``einsum('irs,is->ir', gram_blocks(...), x)``.  ``row_active``
+    (optional int32 per row, device tensor or array): rows with 0 are skipped
+    and return 0."""
+    mode = check_mode(mode, weights.order)
+    x = check_factor(x, rows=weights.shape[mode], name="x")
+    factors, rank = check_factor_list(factors, weights.shape, skip_mode=mode)
+    if x.shape[1] != rank:
+        raise ValueError(f"x rank {x.shape[1]} does not match factor rank {rank}")
+    dtype = _compute_dtype(list(factors) + [x])
+    on_device = _device_mode(list(factors) + [x])
+    torch = _torch()
+    dev = [_to_device(f, dtype) for f in factors]
+    dx = _to_device(x, dtype)
+    out = torch.empty((weights.shape[mode], rank), dtype=dtype, device=cuda_device())
+    act = None
+    if row_active is not None:
+        act = torch.as_tensor(row_active).to(device=cuda_device(), dtype=torch.int32).contiguous()
+        if act.numel() != weights.shape[mode]:
+            raise ValueError("row_active must have one entry per row of the mode")
+    if weights.nnz == 0:
+        out.zero_()
+    else:
+        w = _weights_arg(weights, mode, dtype)
+        _lib.check(_lib.load().cpfit_gram_matvec(
+            weights.device_pattern().handle, mode, _dtype_code(dtype), rank, _vp(w), 1,
+            _ptrs(dev), _vp(dx), _vp(act), _vp(out), _stream()), "gram_matvec")
+    return out if on_device else to_host(out)
+
+
 def solve_factor(weights: SparseTensor, factors, rhs, mode: int, reg: float = 0.0,
                  row_batches: int = 1, stage_rows: int = DEFAULT_STAGE_ROWS,
                  threads: int = 1, return_gram: bool = False):

@@ -72,6 +72,10 @@ class SolverConfig:
     gn_damping: float = 0.0
     gn_damping_decay: float = 0.5
     warmup_sweeps: int = 0
+    # not in the reference: "direct" = its per-row LAPACK solve (batched
+    # Cholesky here); "cg" = Gram-free per-row conjugate gradients (BASELINE
+    # cfg 3 "ALS completion with implicit CG"), stopped by cg_tol / cg_max
+    als_solver: str = "direct"
 
     def __post_init__(self):
         if self.rank < 1:
@@ -97,6 +101,8 @@ class SolverConfig:
             raise ValueError("gn_damping must be >= 0 and its decay in (0, 1]")
         if self.warmup_sweeps < 0:
             raise ValueError("warmup_sweeps must be >= 0")
+        if self.als_solver not in ("direct", "cg"):
+            raise ValueError(f"unknown als_solver {self.als_solver!r}")
 
     def cg_max_iters(self) -> int:
         return self.cg_max if self.cg_max is not None else min(30, 3 * self.rank)
@@ -254,6 +260,83 @@ def _als_mode_device(t: SparseTensor, F, mode: int, reg: float, keep_gram: bool 
     return x
 
 
+def _als_mode_cg_device(t: SparseTensor, F, mode: int, reg: float, tol: float, max_iters: int,
+                        warm_start: bool = True, weights=None, rhs=None):
+    """One least-squares ALS mode update without Gram blocks ("ALS completion
+    with implicit CG", BASELINE cfg 3): rhs = MTTKRP of the data, then every
+    row's (G_i + reg I) x_i = rhs_i by conjugate gradients whose product G_i p_i
+    is one pass over the nonzeros (cpfit_gram_matvec); rows carry their own
+    alpha / beta and drop out of the passes as they converge (pcg_solve's
+    stopping rule, optim.py:521-523, per row).  Warm-started from F[mode].
+    Returns (x, rhs, iterations).  Peak extra memory: five I_n x R arrays
+    instead of the I_n x R x R Gram buffer."""
+    torch = _torch()
+    ref = next(f for n, f in enumerate(F) if f is not None and n != mode)
+    dtype, dev, rank = ref.dtype, ref.device, ref.shape[1]
+    code = _dtype_code(dtype)
+    L = _lib.load()
+    pat = t.device_pattern()
+    rows = t.shape[mode]
+    ptrs = _ptrs([None if n == mode else f for n, f in enumerate(F)])
+    st = _stream()
+    if rhs is None:
+        rhs = torch.empty((rows, rank), dtype=dtype, device=dev)
+        vals = t.sorted_values(mode, dtype) if t.nnz else None
+        _lib.check(L.cpfit_mttkrp(pat.handle, mode, code, rank,
+                                  None if vals is None else ctypes.c_void_p(vals.data_ptr()), 1,
+                                  ptrs, ctypes.c_void_p(rhs.data_ptr()), st), "mttkrp")
+    wptr = None if weights is None else ctypes.c_void_p(weights.data_ptr())
+
+    def matvec(v, active, out):
+        _lib.check(L.cpfit_gram_matvec(pat.handle, mode, code, rank, wptr, 1, ptrs,
+                                       ctypes.c_void_p(v.data_ptr()),
+                                       None if active is None else ctypes.c_void_p(active.data_ptr()),
+                                       ctypes.c_void_p(out.data_ptr()), st), "gram_matvec")
+
+    q = torch.empty_like(rhs)
+    r = torch.empty_like(rhs)
+    p = torch.empty_like(rhs)
+    rho = torch.empty(rows, dtype=torch.float64, device=dev)
+    thresh2 = torch.empty(rows, dtype=torch.float64, device=dev)
+    active = torch.empty(rows, dtype=torch.int32, device=dev)
+    status = torch.zeros(2, dtype=torch.int64, device=dev)
+    if warm_start and F[mode] is not None:
+        x = F[mode].to(dtype).clone()
+        matvec(x, None, q)
+        ax = ctypes.c_void_p(q.data_ptr())
+    else:
+        x = torch.zeros_like(rhs)
+        ax = None
+    vp = lambda a: ctypes.c_void_p(a.data_ptr())  # noqa: E731
+    _lib.check(L.cpfit_cg_rows_init(code, rows, rank, float(reg), float(tol), vp(rhs), ax, vp(x),
+                                    vp(r), vp(p), vp(rho), vp(thresh2), vp(active), vp(status),
+                                    st), "cg_rows_init")
+    iters = 0
+    live, bad = status.tolist()
+    while live and not bad and iters < max_iters:
+        matvec(p, active, q)
+        _lib.check(L.cpfit_cg_rows_step(code, rows, rank, float(reg), vp(q), vp(x), vp(r), vp(p),
+                                        vp(rho), vp(thresh2), vp(active), vp(status), st),
+                   "cg_rows_step")
+        iters += 1
+        live, bad = status.tolist()
+    if bad:
+        raise NumericalError("non-finite curvature inside CG")
+    return x, rhs, iters
+
+
+def _als_ls_cg_device(t: SparseTensor, F, reg: float, tol: float, max_iters: int):
+    """One implicit-CG least-squares ALS sweep on device factors (modes in
+    order, optim.py:194-206).  Returns per-mode (rhs, CG iterations)."""
+    rhss, iters = [], []
+    for mode in range(t.order):
+        x, rhs, it = _als_mode_cg_device(t, F, mode, reg, tol, max_iters)
+        F[mode] = x
+        rhss.append(rhs)
+        iters.append(it)
+    return rhss, iters
+
+
 def _als_ls_device(t: SparseTensor, F, reg: float, keep_gram: bool = True):
     """One least-squares ALS sweep on device factors F (list of CUDA tensors,
     updated in place, modes in order, optim.py:194-206).  Returns per-mode
@@ -276,6 +359,15 @@ def als_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
     (optim.py:180-229)."""
     if generalized is None:
         generalized = loss.ident != "ls"
+    if not generalized and cfg.als_solver == "cg":
+        F = _to_dev_factors(state.factors)
+        rhss, _ = _als_ls_cg_device(t, F, cfg.reg, cfg.cg_tol, cfg.cg_max_iters())
+        host = not any(_is_torch(f) for f in state.factors)
+        for mode in range(t.order):
+            state.ls_gram[mode] = None  # never formed
+            state.ls_rhs[mode] = rhss[mode].cpu().numpy() if host else rhss[mode]
+        _write_back(state.factors, F)
+        return
     if not generalized:
         F = _to_dev_factors(state.factors)
         grams, rhss = _als_ls_device(t, F, cfg.reg)
