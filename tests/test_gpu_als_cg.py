@@ -129,3 +129,27 @@ def test_cg_als_run_driver_and_validation():
     assert np.allclose([r.metric for r in a.records], [r.metric for r in b.records], rtol=1e-7)
     assert np.allclose([r.objective for r in a.records], [r.objective for r in b.records],
                        rtol=1e-7)
+
+
+@pytest.mark.parametrize("rank", [16, 32])
+def test_fragment_gram_rank16_32_zipf_vs_oracle(rank):
+    """The register-fragment Gram kernel at the ranks of cfg 2 / cfg 3 on a
+    Zipf instance with split rows: unit and weighted Grams and one ALS sweep
+    (fused right-hand side) against the oracle."""
+    shape, keys, values = synth.cfg3(nnz=200_000, shape=(4_801, 1_777, 218))
+    t = cp.SparseTensor(shape, keys, values, validate=False)
+    ot = O.OTensor(shape, keys, values)
+    rng = np.random.default_rng(rank)
+    factors = [rng.random((d, rank)) / np.sqrt(rank) for d in shape]
+    for mode in range(3):
+        got = cp.gram_blocks(t.observation_mask(), factors, mode)
+        want = O.gram_blocks(ot.with_values(np.ones(ot.nnz)), factors, mode)
+        assert rel(got, want) < 1e-12
+        gw = cp.gram_blocks(t, factors, mode)  # weighted (sqrt(w) precomputed)
+        assert rel(gw, O.gram_blocks(ot, factors, mode)) < 1e-12
+    st = CompletionState(factors=[f.copy() for f in factors], rng=cp.RngState(0))
+    als_sweep(t, st, get_loss("ls"), SolverConfig(rank=rank, reg=1e-2))
+    fs = [f.copy() for f in factors]
+    O.als_sweep(ot, fs, 1e-2)
+    for n in range(3):
+        assert rel(st.factors[n], fs[n]) < 1e-10
