@@ -70,6 +70,15 @@ int cpfit_pattern_create_coords(int order, const int64_t *dims, int64_t nnz,
 
 int cpfit_pattern_destroy(cpfit_pattern *p);
 
+/* As cpfit_pattern_destroy, but stream-ordered: every buffer is released with
+ * cudaFreeAsync on `stream` and the call never synchronises the device.  The
+ * caller guarantees that all work using the pattern was submitted to `stream`
+ * (the host mirror tracks this per pattern and falls back to
+ * cpfit_pattern_destroy otherwise).  Sampled SGD patterns are created and
+ * destroyed once per step (optim.py:300-330): this keeps that off the
+ * device-wide synchronisation path. */
+int cpfit_pattern_destroy_async(cpfit_pattern *p, void *stream);
+
 int cpfit_pattern_info(const cpfit_pattern *p, int *order, int64_t *nnz);
 
 /* Device pointer to the int32 coordinates of `mode` (canonical order). */

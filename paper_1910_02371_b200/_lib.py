@@ -44,6 +44,7 @@ SYMBOLS = (
     "cpfit_ccsr_spmm", "cpfit_pairwise_tttp", "cpfit_pairwise_fold_sum",
     "cpfit_dense_mttkrp", "cpfit_dense_xc", "cpfit_dense_gram", "cpfit_probe_l2_read",
     "cpfit_gram_matvec", "cpfit_cg_rows_init", "cpfit_cg_rows_step",
+    "cpfit_pattern_destroy_async",
 )
 
 _vp = ctypes.c_void_p
@@ -76,6 +77,7 @@ def load(path: str | None = None):
         "cpfit_pattern_create_coords": [_int, ctypes.POINTER(_i64), _i64, _PP, _vp,
                                         ctypes.POINTER(_vp)],
         "cpfit_pattern_destroy": [_vp],
+        "cpfit_pattern_destroy_async": [_vp, _vp],
         "cpfit_pattern_info": [_vp, ctypes.POINTER(_int), ctypes.POINTER(_i64)],
         "cpfit_pattern_coords": [_vp, _int, ctypes.POINTER(_vp)],
         "cpfit_pattern_set_task_size": [_vp, _i64],

@@ -125,9 +125,25 @@ class DevicePattern:
     def __init__(self, shape, nnz: int, handle: int, task_size: int | None = None):
         self.shape = tuple(shape)
         self.nnz = int(nnz)
-        self.handle = ctypes.c_void_p(handle)
+        self._h = ctypes.c_void_p(handle)
+        self._stream = None      # the one stream every call so far was issued on
+        self._streams_mixed = False
         if task_size is not None:
             _lib.check(_lib.load().cpfit_pattern_set_task_size(self.handle, int(task_size)))
+
+    @property
+    def handle(self):
+        """The C handle.  Every use goes through here, so the pattern knows
+        whether all of its device work was issued on a single stream (then it
+        can be released stream-ordered, without a device synchronisation)."""
+        h = self._h
+        if h is not None:
+            s = current_stream()
+            if self._stream is None:
+                self._stream = s
+            elif self._stream != s:
+                self._streams_mixed = True
+        return h
 
     @classmethod
     def from_keys(cls, shape, keys):
@@ -177,13 +193,16 @@ class DevicePattern:
                 device_view(offs.value, self.shape[mode] + 1, "<i8", self))
 
     def __del__(self):
-        h = getattr(self, "handle", None)
+        h = getattr(self, "_h", None)
         if h is not None and h.value and _lib._lib is not None:
             try:
-                _lib.load().cpfit_pattern_destroy(h)
+                if self._stream is not None and not self._streams_mixed:
+                    _lib.load().cpfit_pattern_destroy_async(h, ctypes.c_void_p(self._stream))
+                else:
+                    _lib.load().cpfit_pattern_destroy(h)
             except Exception:  # interpreter shutdown
                 pass
-            self.handle = None
+            self._h = None
 
 
 @dataclass

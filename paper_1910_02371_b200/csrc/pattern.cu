@@ -638,34 +638,49 @@ int cpfit_pattern_create_coords(int order, const int64_t *dims, int64_t nnz,
   return CPFIT_OK;
 }
 
-int cpfit_pattern_destroy(cpfit_pattern *p) {
-  if (!p) return CPFIT_OK;
-  // stream-ordered frees on the legacy stream after a device sync keep this
-  // safe regardless of which stream last used the buffers
-  cudaDeviceSynchronize();
+// Release every device buffer of a pattern.  stream_ordered: cudaFreeAsync on
+// `s` (no host or device-wide synchronisation); otherwise a device sync and
+// synchronous frees, safe whatever streams used the buffers.
+static void pattern_release(cpfit_pattern *p, bool stream_ordered, cudaStream_t s) {
+  auto rel = [&](void *q) {
+    if (!q) return;
+    if (stream_ordered) cudaFreeAsync(q, s);
+    else cudaFree(q);
+  };
+  if (!stream_ordered) cudaDeviceSynchronize();
   for (int m = 0; m < p->order; ++m) {
     CpfitModeLayout &L = p->modes[m];
-    if (L.perm) cudaFree(L.perm);
-    if (L.offsets) cudaFree(L.offsets);
+    rel(L.perm);
+    rel(L.offsets);
     for (int k = 0; k < p->order; ++k)
-      if (L.owns_sorted[k] && L.sorted_idx[k]) cudaFree(L.sorted_idx[k]);
-    if (L.task_begin) cudaFree(L.task_begin);
-    if (L.task_row) cudaFree(L.task_row);
-    if (L.task_slot) cudaFree(L.task_slot);
-    if (L.split_row) cudaFree(L.split_row);
-    if (L.split_slot) cudaFree(L.split_slot);
-    if (L.identity_perm) cudaFree(L.identity_perm);
+      if (L.owns_sorted[k]) rel(L.sorted_idx[k]);
+    rel(L.task_begin);
+    rel(L.task_row);
+    rel(L.task_slot);
+    rel(L.split_row);
+    rel(L.split_slot);
+    rel(L.identity_perm);
     CpfitModeLayout &C = p->coarse[m];
-    if (C.task_begin) cudaFree(C.task_begin);
-    if (C.task_row) cudaFree(C.task_row);
-    if (C.task_slot) cudaFree(C.task_slot);
-    if (C.split_row) cudaFree(C.split_row);
-    if (C.split_slot) cudaFree(C.split_slot);
+    rel(C.task_begin);
+    rel(C.task_row);
+    rel(C.task_slot);
+    rel(C.split_row);
+    rel(C.split_slot);
   }
-  for (int n = 0; n < p->order; ++n)
-    if (p->coords[n]) cudaFree(p->coords[n]);
-  if (p->parent) cudaFree(p->parent);
+  for (int n = 0; n < p->order; ++n) rel(p->coords[n]);
+  rel(p->parent);
   delete p;
+}
+
+int cpfit_pattern_destroy(cpfit_pattern *p) {
+  if (!p) return CPFIT_OK;
+  pattern_release(p, false, nullptr);
+  return CPFIT_OK;
+}
+
+int cpfit_pattern_destroy_async(cpfit_pattern *p, void *stream) {
+  if (!p) return CPFIT_OK;
+  pattern_release(p, true, (cudaStream_t)stream);
   return CPFIT_OK;
 }
 

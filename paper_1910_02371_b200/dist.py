@@ -237,10 +237,15 @@ class ShardedSGD:
 class DeviceBackend:
     """CUDA kernels + NCCL (factors are CUDA tensors)."""
 
-    def __init__(self):
+    def __init__(self, als_solver: str = "direct", cg_tol: float = 5e-3, cg_max: int = 30):
         import torch
         self.torch = torch
         self.xp = torch
+        if als_solver not in ("direct", "cg"):
+            raise ValueError(f"unknown als_solver {als_solver!r}")
+        self.als_solver = als_solver
+        self.cg_tol = float(cg_tol)
+        self.cg_max = int(cg_max)
 
     def make_shard(self, shape, keys, values):
         from .core import SparseTensor
@@ -248,8 +253,15 @@ class DeviceBackend:
 
     def als_mode(self, shard, factors, mode, reg, lo, hi):
         """Rows lo..hi of the updated factor: MTTKRP + Gram + solve on the shard,
-        with the shard's own (rebased) mode factor slot unused."""
-        from .optim import _als_mode_device
+        with the shard's own (rebased) mode factor slot unused -- or, with
+        als_solver="cg", the Gram-free per-row CG update warm-started from the
+        block's current rows (SolverConfig.als_solver)."""
+        from .optim import _als_mode_cg_device, _als_mode_device
+        if self.als_solver == "cg":
+            local = list(factors)
+            local[mode] = factors[mode][lo:hi].contiguous()
+            x, _, _ = _als_mode_cg_device(shard, local, mode, reg, self.cg_tol, self.cg_max)
+            return x
         return _als_mode_device(shard, factors, mode, reg, row_offset=lo)
 
     def make_nnz_shard(self, shape, keys, values):

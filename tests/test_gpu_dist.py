@@ -53,6 +53,17 @@ def test_sharded_als_device_backend_single_rank():
         _als_ls_device(t, F2, 1e-5, keep_gram=False)
         for a, b in zip(F1, F2):
             assert torch.equal(a, b)
+        # implicit-CG solver through the same sharding: equals the unsharded
+        # CG sweep bit for bit (same kernels, rebased rows)
+        from paper_1910_02371_b200.optim import _als_ls_cg_device
+        alsc = D.ShardedALS(coords, vals, shape, 1e-5,
+                            D.DeviceBackend(als_solver="cg", cg_tol=1e-6, cg_max=48))
+        F3 = [f.clone() for f in init]
+        alsc.sweep(F3)
+        F4 = [f.clone() for f in init]
+        _als_ls_cg_device(t, F4, 1e-5, 1e-6, 48)
+        for a, b in zip(F3, F4):
+            assert torch.equal(a, b)
     finally:
         dist.destroy_process_group()
 
