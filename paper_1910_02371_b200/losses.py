@@ -269,9 +269,20 @@ def fast_ls_loss(t_norm_sq: float, u_new, g_blocks, p_rhs) -> float:
             raise ValueError("g_blocks shape does not match the updated factor")
         if tuple(p.shape) != tuple(u.shape):
             raise ValueError("p_rhs shape does not match the updated factor")
-        u, g, p = u.double(), g.double(), p.double()
-        quad = float(torch.einsum("ir,irs,is->", u, g, u))
-        cross = float((u * p).sum())
+        u, g, p = u.double().contiguous(), g.double().contiguous(), p.double().contiguous()
+        rank = u.shape[1]
+        if rank <= 32:
+            # G_i u_i by the batched symmetric mat-vec kernel, then two
+            # fixed-order device dot products (no library contraction)
+            gu = torch.empty_like(u)
+            _lib.check(_lib.load().cpfit_batched_symv(
+                _dtype_code(u.dtype), rank, u.shape[0], ctypes.c_void_p(g.data_ptr()),
+                ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(gu.data_ptr()),
+                ctypes.c_void_p(current_stream())), "batched_symv")
+            quad = _reduce(2, u, gu)
+        else:
+            quad = float(torch.einsum("ir,irs,is->", u, g, u))
+        cross = _reduce(2, u, p)
         return float(t_norm_sq) + quad - 2.0 * cross
     u_new = np.asarray(u_new, dtype=np.float64)
     if g_blocks.shape != (u_new.shape[0], u_new.shape[1], u_new.shape[1]):

@@ -223,6 +223,11 @@ def test_fast_ls_loss_identity():
         fast = fast_ls_loss(float(np.sum(t.values ** 2)), new0, gram, rhs)
         direct = objective(get_loss("ls"), t, factors, reg=0.0)
         assert fast == pytest.approx(direct, rel=1e-10)
+        # device tensors: batched symmetric mat-vec + fixed-order dots
+        import torch
+        fast_dev = fast_ls_loss(float(np.sum(t.values ** 2)), torch.from_numpy(new0).cuda(),
+                                torch.from_numpy(gram).cuda(), torch.from_numpy(rhs).cuda())
+        assert fast_dev == pytest.approx(fast, rel=1e-12)
 
 
 def test_cfg2_scaled_sweeps_vs_oracle():
