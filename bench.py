@@ -223,8 +223,11 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE cfg 2 shape)",
-        "config": CONFIG,
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE cfg 2 shape/value laws)",
+        # same config block as the GPU arm (the same synth.cfg2() tensor, seed 2);
+        # with --gpus N the GPU arm shards this one tensor by nonzero ranges
+        "config": dict(CONFIG, parallelism=f"nnz-shard{args.gpus}" if args.gpus > 1 else "1gpu"),
         "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": threads, "kind": "port",
                          "sample": f"full cfg 2 workload, {args.steps} steps after "
                                    f"{args.warmup} warm-up (oracle/cpfit_oracle.c, OpenMP)"},
