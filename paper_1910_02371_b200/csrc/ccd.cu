@@ -235,19 +235,19 @@ struct CcdBatch {
 };
 
 // Stream loads of one batch (U warp steps of 32 entries) of chunk c.
-template <int NO, int U, bool FOLD>
+template <int NO, int U, bool FOLD, int MODE>
 __device__ __forceinline__ void ccd_load_batch(const CcdParams &p, int64_t c, int b, int lane,
                                                CcdBatch<NO, U> &B) {
   const int64_t c0 = c * CCD_FLAT_CHUNK;
   const int64_t c1 = min(c0 + (int64_t)CCD_FLAT_CHUNK, p.nnz);
-  const int32_t *__restrict__ key = p.sidx[p.mode];
+  const int32_t *__restrict__ key = p.sidx[MODE];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int64_t e = c0 + (int64_t)b * 32 * U + 32 * u + lane;
     const bool ok = e < c1;
     B.row[u] = ok ? __ldg(key + e) : -2;
 #pragma unroll
-    for (int q = 0; q < NO; ++q) B.ix[u][q] = (ok && q != p.mode) ? __ldg(p.sidx[q] + e) : 0;
+    for (int q = 0; q < NO; ++q) B.ix[u][q] = (ok && q != MODE) ? __ldg(p.sidx[q] + e) : 0;
     if constexpr (FOLD) {
       B.rh[u] = ok ? __ldg(p.rhat + e) : 0.0;
       B.pe[u] = 0;
@@ -258,7 +258,10 @@ __device__ __forceinline__ void ccd_load_batch(const CcdParams &p, int64_t c, in
   }
 }
 
-template <int NO, bool FOLD>
+// MODE is a template parameter: with a run-time mode every `q == mode` test in
+// the unrolled per-mode loops became ISETP / FSEL / constant-bank pointer
+// loads (cfg 3 pass 1.14 -> 1.09 ms at R = 4).
+template <int NO, bool FOLD, int MODE>
 __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_t nchunks,
                                                        double2 *__restrict__ pf,
                                                        double2 *__restrict__ pl) {
@@ -266,12 +269,12 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int32_t *__restrict__ key = p.sidx[p.mode];
-  const int mode = p.mode;
+  const int32_t *__restrict__ key = p.sidx[MODE];
+  constexpr int mode = MODE;
   int64_t c = warp;
   int bi = 0;
   CcdBatch<NO, U> cur;
-  if (c < nchunks) ccd_load_batch<NO, U, FOLD>(p, c, 0, lane, cur);
+  if (c < nchunks) ccd_load_batch<NO, U, FOLD, MODE>(p, c, 0, lane, cur);
   int32_t first_row = 0, last_row = 0, carry_row = -1;
   bool first_cont = false, last_cont = false;
   double la = 0.0, lb = 0.0;  // this lane's share of the carried row's (num, den)
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
       nc = c + nwarps;
     }
     CcdBatch<NO, U> nxt;
-    if (nc < nchunks) ccd_load_batch<NO, U, FOLD>(p, nc, nb, lane, nxt);
+    if (nc < nchunks) ccd_load_batch<NO, U, FOLD, MODE>(p, nc, nb, lane, nxt);
     // gathers (factor columns; rhat through the permutation unless FOLD)
     double g[U][NO], sv[U][NO], av[U][NO], rh[U];
 #pragma unroll
@@ -475,6 +478,36 @@ static int ccd_path(cpfit_pattern *pt) {
   return pt->order >= 2 && pt->order <= 5 ? CCD_PATH_FLAT : CCD_PATH_TASK;
 }
 
+namespace cpfit {
+template <int NO, int M>
+static int launch_ccd_flat_mode(int mode, bool fold, unsigned grid, cudaStream_t s,
+                                const CcdParams &p, int64_t nchunks, double2 *pf, double2 *pl) {
+  if constexpr (M < NO) {
+    if (mode == M) {
+      if (fold) ccd_flat_kernel<NO, true, M><<<grid, 256, 0, s>>>(p, nchunks, pf, pl);
+      else ccd_flat_kernel<NO, false, M><<<grid, 256, 0, s>>>(p, nchunks, pf, pl);
+      return CPFIT_OK;
+    }
+    return launch_ccd_flat_mode<NO, M + 1>(mode, fold, grid, s, p, nchunks, pf, pl);
+  } else {
+    set_error("mode %d out of range", mode);
+    return CPFIT_EINVAL;
+  }
+}
+
+static int launch_ccd_flat(int order, int mode, bool fold, unsigned grid, cudaStream_t s,
+                           const CcdParams &p, int64_t nchunks, double2 *pf, double2 *pl) {
+  switch (order) {
+    case 2: return launch_ccd_flat_mode<2, 0>(mode, fold, grid, s, p, nchunks, pf, pl);
+    case 3: return launch_ccd_flat_mode<3, 0>(mode, fold, grid, s, p, nchunks, pf, pl);
+    case 4: return launch_ccd_flat_mode<4, 0>(mode, fold, grid, s, p, nchunks, pf, pl);
+    case 5: return launch_ccd_flat_mode<5, 0>(mode, fold, grid, s, p, nchunks, pf, pl);
+  }
+  set_error("order %d has no flat CCD++ kernel", order);
+  return CPFIT_EINVAL;
+}
+}  // namespace cpfit
+
 extern "C" {
 
 int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rhat,
@@ -540,15 +573,7 @@ int cpfit_ccd_step(cpfit_pattern *pt, int mode, double *const *cols, double *rha
     CPFIT_TRY(pf.alloc(nchunks));
     CPFIT_TRY(pl.alloc(nchunks));
     const unsigned grid = grid_for(nchunks * 32, 256);
-#define CCD_FLAT_CASE(NO)                                                      \
-  if (pt->order == NO) {                                                       \
-    if (fold)                                                                  \
-      ccd_flat_kernel<NO, true><<<grid, 256, 0, s>>>(p, nchunks, pf.ptr, pl.ptr);  \
-    else                                                                       \
-      ccd_flat_kernel<NO, false><<<grid, 256, 0, s>>>(p, nchunks, pf.ptr, pl.ptr); \
-  }
-    CCD_FLAT_CASE(2) CCD_FLAT_CASE(3) CCD_FLAT_CASE(4) CCD_FLAT_CASE(5)
-#undef CCD_FLAT_CASE
+    CPFIT_TRY(launch_ccd_flat(pt->order, mode, fold, grid, s, p, nchunks, pf.ptr, pl.ptr));
     CPFIT_LAUNCH_CHECK("ccd_flat");
     ccd_flat_fixup<<<grid_for(p.dim * 32, 256), 256, 0, s>>>(p, L.offsets, pf.ptr, pl.ptr);
     CPFIT_LAUNCH_CHECK("ccd_flat_fixup");
