@@ -23,6 +23,8 @@ KEYS = [
     ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
      "DMMA pipe %"),
     ("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed", "L1 LSU wavefronts %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram %peak"),
 ]
 
 
