@@ -261,7 +261,8 @@ __device__ __forceinline__ void ccd_load_batch(const CcdParams &p, int64_t c, in
 // MODE is a template parameter: with a run-time mode every `q == mode` test in
 // the unrolled per-mode loops became ISETP / FSEL / constant-bank pointer
 // loads (cfg 3 pass 1.14 -> 1.09 ms at R = 4).
-template <int NO, bool FOLD, int MODE>
+// HS / HA: the fold's sub / add sides as template flags too.
+template <int NO, bool FOLD, int MODE, bool HS = false, bool HA = false>
 __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_t nchunks,
                                                        double2 *__restrict__ pf,
                                                        double2 *__restrict__ pl) {
@@ -309,10 +310,10 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
         const int32_t iq = q == mode ? rw : cur.ix[u][q];
         g[u][q] = q != mode ? __ldg(p.cols[q] + iq) : 1.0;
         if constexpr (FOLD) {
-          sv[u][q] = p.has_sub ? __ldg(p.sub[q] + iq) : 0.0;
+          sv[u][q] = HS ? __ldg(p.sub[q] + iq) : 0.0;
           // modes after this one are not updated yet in this column: their
           // pre-sweep value is the current one (no second gather)
-          av[u][q] = !p.has_add ? 0.0 : (q > mode ? g[u][q] : __ldg(p.add[q] + iq));
+          av[u][q] = !HA ? 0.0 : (q > mode ? g[u][q] : __ldg(p.add[q] + iq));
         }
       }
       if constexpr (FOLD) {
@@ -334,20 +335,20 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
         // the reference's orders (sub: modes ascending; add: partial over
         // p != 0, then col_0) -- identical in every mode's copy
         double r = rh[u];
-        if (p.has_sub) {
+        if (HS) {
           double sp = sv[u][0];
 #pragma unroll
           for (int q = 1; q < NO; ++q) sp = __dmul_rn(sp, sv[u][q]);
           r = __dsub_rn(r, sp);
         }
-        if (p.has_add) {
+        if (HA) {
           double ap = 1.0;
 #pragma unroll
           for (int q = 1; q < NO; ++q) ap = __dmul_rn(ap, av[u][q]);
           r = __dadd_rn(r, __dmul_rn(ap, av[u][0]));
         }
         const int64_t e = c0 + (int64_t)bi * 32 * U + 32 * u + lane;
-        if (cur.row[u] >= 0) p.rhat[e] = r;
+        if cur.row[u] >= 0 p.rhat[e] = r;
         rh[u] = r;
       }
       w1[u] = cur.row[u] >= 0 ? __dmul_rn(rh[u], part) : 0.0;
@@ -484,8 +485,13 @@ static int launch_ccd_flat_mode(int mode, bool fold, unsigned grid, cudaStream_t
                                 const CcdParams &p, int64_t nchunks, double2 *pf, double2 *pl) {
   if constexpr (M < NO) {
     if (mode == M) {
-      if (fold) ccd_flat_kernel<NO, true, M><<<grid, 256, 0, s>>>(p, nchunks, pf, pl);
-      else ccd_flat_kernel<NO, false, M><<<grid, 256, 0, s>>>(p, nchunks, pf, pl);
+      if (!fold) ccd_flat_kernel<NO, false, M><<<grid, 256, 0, s>>>(p, nchunks, pf, pl);
+      else if (p.has_sub && p.has_add)
+        ccd_flat_kernel<NO, true, M, true, true><<<grid, 256, 0, s>>>(p, nchunks, pf, pl);
+      else if (p.has_sub)
+        ccd_flat_kernel<NO, true, M, true, false><<<grid, 256, 0, s>>>(p, nchunks, pf, pl);
+      else
+        ccd_flat_kernel<NO, true, M, false, true><<<grid, 256, 0, s>>>(p, nchunks, pf, pl);
       return CPFIT_OK;
     }
     return launch_ccd_flat_mode<NO, M + 1>(mode, fold, grid, s, p, nchunks, pf, pl);
