@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(256) ccd_flat_kernel(const CcdParams p, int64_
           r = __dadd_rn(r, __dmul_rn(ap, av[u][0]));
         }
         const int64_t e = c0 + (int64_t)bi * 32 * U + 32 * u + lane;
-        if cur.row[u] >= 0 p.rhat[e] = r;
+        if (cur.row[u] >= 0) p.rhat[e] = r;
         rh[u] = r;
       }
       w1[u] = cur.row[u] >= 0 ? __dmul_rn(rh[u], part) : 0.0;
