@@ -32,11 +32,22 @@
 #ifndef CPFIT_MTTKRP_MINB_F32
 #define CPFIT_MTTKRP_MINB_F32 3  // fp32 (cfg 5 SGD samples: 4 cost ~1 ms per step)
 #endif
+#ifndef CPFIT_TTTP_MINB_F32
+#define CPFIT_TTTP_MINB_F32 4  // fp32 (cfg 5-like 2e7 nnz: 1.078 -> 0.865 ms with U0 = 2)
+#endif
 #ifndef CPFIT_TTTP_U0
 #define CPFIT_TTTP_U0 4  // TTTP sub-iterations in flight when the mode-0 row is hoisted
 #endif
+#ifndef CPFIT_TTTP_U0_F32
+#define CPFIT_TTTP_U0_F32 2
+#endif
 #ifndef CPFIT_MTTKRP_U
-#define CPFIT_MTTKRP_U 4  // sub-iterations of gathers in flight per MTTKRP round
+#define CPFIT_MTTKRP_U 4  // sub-iterations of gathers in flight per MTTKRP round (fp32)
+#endif
+#ifndef CPFIT_MTTKRP_U64
+// fp64: 2 (cfg 2 0.1657 -> 0.1615 ms, cfg 3-like mode 0 0.766 -> 0.706 ms; 8 is 3-13 %
+// slower, 1 is 12 % slower; fp32 prefers 4: profiles/r2_tuning.md)
+#define CPFIT_MTTKRP_U64 2
 #endif
 #ifndef CPFIT_MTTKRP_KVT64
 #define CPFIT_MTTKRP_KVT64 1
@@ -141,7 +152,8 @@ __device__ __forceinline__ void gather_product(const T *const (&fq)[NPM],
 // nonzero.  Values and outputs are accessed in that permuted but coalesced
 // order.
 template <typename T, int VEC, int LPE, int KV, int NP, bool FULL>
-__global__ void __launch_bounds__(256, CPFIT_TTTP_MINB) tttp_kernel(const TttpParams<T> p) {
+__global__ void __launch_bounds__(256, sizeof(T) == 8 ? CPFIT_TTTP_MINB : CPFIT_TTTP_MINB_F32)
+    tttp_kernel(const TttpParams<T> p) {
   constexpr int G = 32 / LPE;                      // nonzeros per warp step
   constexpr int NPM = NP > 0 ? NP : CPFIT_MAXN;    // register slots for indices
   constexpr int U = NP > 0 ? (LPE < 4 ? LPE : 4) : 1;
@@ -200,7 +212,9 @@ __global__ void __launch_bounds__(256, CPFIT_TTTP_MINB) tttp_kernel(const TttpPa
             }
           }
         }
-        constexpr int U0 = U * CPFIT_TTTP_U0 / 4 <= LPE ? U * CPFIT_TTTP_U0 / 4 : LPE;
+        constexpr int U0M = sizeof(T) == 8 ? CPFIT_TTTP_U0 : CPFIT_TTTP_U0_F32;
+        constexpr int U0S = U * U0M / 4 < 1 ? 1 : U * U0M / 4;
+        constexpr int U0 = U0S <= LPE ? U0S : LPE;
 #pragma unroll
         for (int s0 = 0; s0 < LPE; s0 += U0) {
           T x[U0][NPM][KV][VEC];
@@ -324,7 +338,8 @@ __global__ void __launch_bounds__(256, sizeof(T) == 8 ? CPFIT_MTTKRP_MINB : CPFI
     mttkrp_kernel(const MttkrpParams<T> p) {
   constexpr int G = 32 / LPE;
   constexpr int NPM = NP > 0 ? NP : CPFIT_MAXN;
-  constexpr int U = NP > 0 ? (LPE < CPFIT_MTTKRP_U ? LPE : CPFIT_MTTKRP_U) : 1;
+  constexpr int UT = sizeof(T) == 8 ? CPFIT_MTTKRP_U64 : CPFIT_MTTKRP_U;
+  constexpr int U = NP > 0 ? (LPE < UT ? LPE : UT) : 1;
   const int np = NP > 0 ? NP : p.np;
   const int lane = threadIdx.x & 31;
   const int g = lane / LPE, q = lane % LPE;
