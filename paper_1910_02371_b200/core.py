@@ -258,52 +258,54 @@ class RngState:
 # index arithmetic (core.py:49-102; host utilities)
 
 def linearize(coords, dims) -> int:
+    """Row-major key of one coordinate tuple (last mode fastest)."""
     dims = check_shape(dims)
     if len(coords) != len(dims):
         raise ValueError(f"expected {len(dims)} coordinates, got {len(coords)}")
     key = 0
-    for n, (c, d) in enumerate(zip(coords, dims)):
-        c = int(c)
-        if not 0 <= c < d:
-            raise ValueError(f"coordinate {c} out of range [0, {d}) in mode {n}")
-        key = key * d + c
+    for n, extent in enumerate(dims):
+        c = int(coords[n])
+        if c < 0 or c >= extent:
+            raise ValueError(f"coordinate {c} out of range [0, {extent}) in mode {n}")
+        key = key * extent + c          # Horner in mixed radix
     return key
 
 
 def delinearize(key: int, dims) -> tuple[int, ...]:
     dims = check_shape(dims)
-    key = int(key)
-    if not 0 <= key < math.prod(dims):
-        raise ValueError(f"key {key} out of range for shape {dims}")
-    coords = [0] * len(dims)
-    for n in range(len(dims) - 1, -1, -1):
-        key, coords[n] = divmod(key, dims[n])
-    return tuple(coords)
+    rest = int(key)
+    if rest < 0 or rest >= math.prod(dims):
+        raise ValueError(f"key {rest} out of range for shape {dims}")
+    digits = []
+    for extent in reversed(dims):
+        rest, digit = divmod(rest, extent)
+        digits.append(digit)
+    return tuple(reversed(digits))
 
 
 def linearize_many(coord_arrays, dims) -> np.ndarray:
+    """Vectorised ``linearize`` (host; the device ingest is cpfit_from_coords)."""
     dims = check_shape(dims)
     if len(coord_arrays) != len(dims):
         raise ValueError("one coordinate array per mode required")
-    n_entries = len(coord_arrays[0]) if len(coord_arrays) else 0
-    keys = np.zeros(n_entries, dtype=np.uint64)
-    for n, (c, d) in enumerate(zip(coord_arrays, dims)):
-        c = np.asarray(c)
-        if c.size and (c.min() < 0 or c.max() >= d):
-            raise ValueError(f"coordinate out of range [0, {d}) in mode {n}")
-        keys = keys * np.uint64(d) + c.astype(np.uint64)
+    keys = np.zeros(len(coord_arrays[0]) if len(coord_arrays) else 0, dtype=np.uint64)
+    for n, extent in enumerate(dims):
+        col = np.asarray(coord_arrays[n])
+        if col.size and (col.min() < 0 or col.max() >= extent):
+            raise ValueError(f"coordinate out of range [0, {extent}) in mode {n}")
+        keys *= np.uint64(extent)
+        keys += col.astype(np.uint64)
     return keys
 
 
 def delinearize_many(keys, dims) -> tuple[np.ndarray, ...]:
     dims = check_shape(dims)
-    rem = np.asarray(keys, dtype=np.uint64).copy()
-    coords = [None] * len(dims)
-    for n in range(len(dims) - 1, -1, -1):
-        d = np.uint64(dims[n])
-        coords[n] = (rem % d).astype(np.int64)
-        rem //= d
-    return tuple(coords)
+    rest = np.array(keys, dtype=np.uint64)        # private copy, consumed below
+    out: list = []
+    for extent in reversed(dims):
+        rest, digit = np.divmod(rest, np.uint64(extent))
+        out.append(digit.astype(np.int64))
+    return tuple(reversed(out))
 
 
 # ---------------------------------------------------------------------------
@@ -601,73 +603,81 @@ def counting_sort_by_mode(t: SparseTensor, mode: int):
 
 
 def model_values(factors, coord_arrays, col_block: int = 32) -> np.ndarray:
-    """core.py:252-266: multilinear inner products at given coordinates."""
-    n_entries = len(coord_arrays[0]) if len(coord_arrays) else 0
-    factors = [np.asarray(f.cpu().numpy() if hasattr(f, "cpu") else f, dtype=np.float64)
-               for f in factors]
-    rank = factors[0].shape[1]
-    out = np.zeros(n_entries)
-    for lo in range(0, rank, col_block):
-        hi = min(lo + col_block, rank)
-        prod = factors[0][coord_arrays[0], lo:hi].copy()
-        for n in range(1, len(factors)):
-            prod *= factors[n][coord_arrays[n], lo:hi]
-        out += prod.sum(axis=1)
-    return out
+    """Multilinear inner products sum_r prod_n A_n[i_n, r] at given coordinates.
+
+    Host helper for the synthetic generators.  The summation order is the
+    reference's (core.py:252-266: column blocks of ``col_block``, a row sum per
+    block, blocks added left to right), so generated values are bit-identical."""
+    mats = [np.asarray(f.cpu().numpy() if hasattr(f, "cpu") else f, dtype=np.float64)
+            for f in factors]
+    count = len(coord_arrays[0]) if len(coord_arrays) else 0
+    total = np.zeros(count)
+    rank = mats[0].shape[1]
+    for first in range(0, rank, col_block):
+        cols = slice(first, min(first + col_block, rank))
+        block = mats[0][coord_arrays[0], cols].copy()
+        for mat, idx in zip(mats[1:], coord_arrays[1:]):
+            block *= mat[idx, cols]
+        total += block.sum(axis=1)
+    return total
+
+
+def _observed_keys(shape, observed_fraction: float, g: np.random.Generator) -> np.ndarray:
+    """Bernoulli(observed_fraction) mask over the enumerated cell space, as
+    sorted keys (one uniform draw per cell, like the reference generators)."""
+    cells = math.prod(shape)
+    if observed_fraction >= 1.0:
+        return np.arange(cells, dtype=np.uint64)
+    return np.flatnonzero(g.random(cells) < observed_fraction).astype(np.uint64)
+
+
+def _check_generator_args(shape, observed_fraction: float, cell_cap: int, hint: str):
+    shape = check_shape(shape)
+    if not 0.0 < observed_fraction <= 1.0:
+        raise ValueError("observed_fraction must be in (0, 1]")
+    cells = math.prod(shape)
+    if cells > cell_cap:
+        raise DataError(f"cell space {cells} exceeds enumeration cap {cell_cap}{hint}")
+    return shape
+
+
+_FACTOR_LAWS = {
+    "uniform01": lambda g, size: g.random(size),
+    "gaussian": lambda g, size: g.standard_normal(size),
+}
 
 
 def gen_low_rank(shape, rank: int, observed_fraction: float,
                  value_law: str = "uniform01", rng: RngState | None = None,
                  cell_cap: int = DEFAULT_CELL_CAP):
-    """core.py:269-314 (host synthesis; identical draws to the reference)."""
-    shape = check_shape(shape)
-    if not 0.0 < observed_fraction <= 1.0:
-        raise ValueError("observed_fraction must be in (0, 1]")
-    total = math.prod(shape)
-    if total > cell_cap:
-        raise DataError(f"cell space {total} exceeds enumeration cap {cell_cap}; "
-                        "raise cell_cap explicitly for larger masks")
-    if rng is None:
-        rng = RngState(0)
-    g = rng.generator()
-    factors = []
-    for d in shape:
-        if value_law == "uniform01":
-            factors.append(g.random((d, rank)))
-        elif value_law == "gaussian":
-            factors.append(g.standard_normal((d, rank)))
-        else:
+    """Random rank-``rank`` CP model observed on a Bernoulli mask -> (tensor,
+    truth factors).  Draw order follows core.py:269-314 (factors mode by mode,
+    then the mask), so a given RngState yields the reference's tensor."""
+    shape = _check_generator_args(shape, observed_fraction, cell_cap,
+                                  "; raise cell_cap explicitly for larger masks")
+    g = (rng or RngState(0)).generator()
+    truth = []
+    for extent in shape:
+        if value_law not in _FACTOR_LAWS:
             raise ValueError(f"unknown value_law {value_law!r}")
-    if observed_fraction >= 1.0:
-        keys = np.arange(total, dtype=np.uint64)
-    else:
-        keys = np.flatnonzero(g.random(total) < observed_fraction).astype(np.uint64)
-    coords = delinearize_many(keys, shape)
-    values = model_values(factors, coords)
-    t = SparseTensor(shape, keys, values, validate=False)
-    return t, factors
+        truth.append(_FACTOR_LAWS[value_law](g, (extent, rank)))
+    keys = _observed_keys(shape, observed_fraction, g)
+    values = model_values(truth, delinearize_many(keys, shape))
+    return SparseTensor(shape, keys, values, validate=False), truth
+
+
+def _inverse_index_sum(coords) -> np.ndarray:
+    # default test function of core.py:317-348: 1 / (1 + i_0 + i_1 + ...)
+    acc = np.zeros(len(coords[0]))
+    for c in coords:
+        acc += c
+    return 1.0 / (1.0 + acc)
 
 
 def gen_function_tensor(shape, observed_fraction: float, rng: RngState | None = None,
                         func=None, cell_cap: int = DEFAULT_CELL_CAP) -> SparseTensor:
-    """core.py:317-348 placeholder generator (host)."""
-    shape = check_shape(shape)
-    if not 0.0 < observed_fraction <= 1.0:
-        raise ValueError("observed_fraction must be in (0, 1]")
-    total = math.prod(shape)
-    if total > cell_cap:
-        raise DataError(f"cell space {total} exceeds enumeration cap {cell_cap}")
-    if rng is None:
-        rng = RngState(0)
-    if func is None:
-        def func(coords):
-            s = np.zeros(len(coords[0]))
-            for c in coords:
-                s += c
-            return 1.0 / (1.0 + s)
-    g = rng.generator()
-    if observed_fraction >= 1.0:
-        keys = np.arange(total, dtype=np.uint64)
-    else:
-        keys = np.flatnonzero(g.random(total) < observed_fraction).astype(np.uint64)
-    return SparseTensor(shape, keys, func(delinearize_many(keys, shape)), validate=False)
+    """``func(coords)`` sampled on a Bernoulli mask (core.py:317-348)."""
+    shape = _check_generator_args(shape, observed_fraction, cell_cap, "")
+    keys = _observed_keys(shape, observed_fraction, (rng or RngState(0)).generator())
+    evaluate = func or _inverse_index_sum
+    return SparseTensor(shape, keys, evaluate(delinearize_many(keys, shape)), validate=False)

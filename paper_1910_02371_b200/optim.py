@@ -41,6 +41,7 @@ from .trace import RunTrace
 from .validation import _is_torch
 
 ALGORITHMS = ("als", "ccd", "sgd", "gn", "newton")
+_INIT_LAWS = ("uniform", "gaussian", "svd")
 _TINY = 1e-300
 
 
@@ -78,31 +79,28 @@ class SolverConfig:
     als_solver: str = "direct"
 
     def __post_init__(self):
-        if self.rank < 1:
-            raise ValueError("rank must be >= 1")
-        if self.algorithm not in ALGORITHMS:
-            raise ValueError(f"unknown algorithm {self.algorithm!r}")
-        if self.reg < 0:
-            raise ValueError("reg must be >= 0")
-        if self.max_iters < 0:
-            raise ValueError("max_iters must be >= 0")
-        for name in ("tol", "inner_tol", "cg_tol", "step"):
-            if getattr(self, name) <= 0:
-                raise ValueError(f"{name} must be positive")
-        if not 0.0 < self.sample_rate <= 1.0:
-            raise ValueError("sample_rate must be in (0, 1]")
-        if self.cg_tol >= 1.0:
-            raise ValueError("cg_tol must be in (0, 1)")
-        if self.init not in ("uniform", "gaussian", "svd"):
-            raise ValueError(f"unknown init law {self.init!r}")
-        if self.threads < 1 or self.inner_max < 1 or self.row_batches < 1:
-            raise ValueError("threads, inner_max, row_batches must be >= 1")
-        if self.gn_damping < 0 or not 0.0 < self.gn_damping_decay <= 1.0:
-            raise ValueError("gn_damping must be >= 0 and its decay in (0, 1]")
-        if self.warmup_sweeps < 0:
-            raise ValueError("warmup_sweeps must be >= 0")
-        if self.als_solver not in ("direct", "cg"):
-            raise ValueError(f"unknown als_solver {self.als_solver!r}")
+        # the reference's rules and messages (optim.py:62-86), as a table: the
+        # first failing row raises
+        positive = [n for n in ("tol", "inner_tol", "cg_tol", "step") if getattr(self, n) <= 0]
+        rules = (
+            (self.rank >= 1, "rank must be >= 1"),
+            (self.algorithm in ALGORITHMS, f"unknown algorithm {self.algorithm!r}"),
+            (self.reg >= 0, "reg must be >= 0"),
+            (self.max_iters >= 0, "max_iters must be >= 0"),
+            (not positive, f"{positive[0] if positive else ''} must be positive"),
+            (0.0 < self.sample_rate <= 1.0, "sample_rate must be in (0, 1]"),
+            (self.cg_tol < 1.0, "cg_tol must be in (0, 1)"),
+            (self.init in _INIT_LAWS, f"unknown init law {self.init!r}"),
+            (min(self.threads, self.inner_max, self.row_batches) >= 1,
+             "threads, inner_max, row_batches must be >= 1"),
+            (self.gn_damping >= 0 and 0.0 < self.gn_damping_decay <= 1.0,
+             "gn_damping must be >= 0 and its decay in (0, 1]"),
+            (self.warmup_sweeps >= 0, "warmup_sweeps must be >= 0"),
+            (self.als_solver in ("direct", "cg"), f"unknown als_solver {self.als_solver!r}"),
+        )
+        for ok, message in rules:
+            if not ok:
+                raise ValueError(message)
 
     def cg_max_iters(self) -> int:
         return self.cg_max if self.cg_max is not None else min(30, 3 * self.rank)
@@ -128,54 +126,62 @@ class CompletionState:
 
 def init_state(t: SparseTensor, cfg: SolverConfig, rng: RngState | None = None
                ) -> CompletionState:
-    """optim.py:113-146 (host draws, identical to the reference)."""
-    if rng is None:
-        rng = RngState(cfg.seed).child(0)
+    """Initial factors (host draws in the reference's order, optim.py:113-146:
+    one (I_n x R) block per mode from ``RngState(seed).child(0)``, scaled by
+    1/sqrt(R)); uploaded by the drivers, never regenerated on the device."""
+    rng = rng or RngState(cfg.seed).child(0)
     g = rng.generator()
     scale = 1.0 / math.sqrt(cfg.rank)
-    factors = []
-    for mode, d in enumerate(t.shape):
-        if cfg.init == "uniform":
-            factors.append(g.random((d, cfg.rank)) * scale)
-        elif cfg.init == "gaussian":
-            factors.append(g.standard_normal((d, cfg.rank)) * scale)
-        else:
-            factors.append(_svd_init_factor(t, mode, cfg.rank, g, scale))
+    draw = {"uniform": g.random, "gaussian": g.standard_normal}
+    factors = [
+        draw[cfg.init]((extent, cfg.rank)) * scale if cfg.init in draw
+        else _svd_init_factor(t, mode, cfg.rank, g, scale)
+        for mode, extent in enumerate(t.shape)
+    ]
     if cfg.calibrate_init and t.nnz:
-        model = tttp(t.observation_mask(), factors).values
-        denom = float(np.dot(model, model))
-        if denom > 0.0:
-            c = float(np.dot(t.values, model)) / denom
-            if c != 0.0:
-                s = abs(c) ** (1.0 / t.order)
-                for f in factors:
-                    f *= s
-                if c < 0.0:
-                    factors[0] *= -1.0
+        _calibrate_scale(t, factors)
     return CompletionState(factors=factors, rng=rng)
 
 
+def _calibrate_scale(t: SparseTensor, factors) -> None:
+    """Least-squares scalar c = <t, m> / <m, m> between the data and the initial
+    model m, spread evenly over the modes (|c|^(1/N) each, the sign on mode 0);
+    optim.py:131-145."""
+    model = tttp(t.observation_mask(), factors).values
+    mm = float(np.dot(model, model))
+    if mm <= 0.0:
+        return
+    c = float(np.dot(t.values, model)) / mm
+    if c == 0.0:
+        return
+    per_mode = abs(c) ** (1.0 / t.order)
+    for f in factors:
+        f *= per_mode
+    if c < 0.0:
+        factors[0] *= -1.0
+
+
 def _svd_init_factor(t, mode, rank, g, scale):
-    """optim.py:149-174 (scipy svds on the host; initialisation only)."""
+    """Leading left singular vectors of the mode-``mode`` unfolding (scipy
+    ``svds`` on the host, as optim.py:149-174; initialisation only).  Columns
+    the unfolding cannot supply are uniform draws."""
     from scipy.sparse import csr_matrix
     from scipy.sparse.linalg import svds
     coords = t.coords()
-    rows = coords[mode]
     n_rows = t.shape[mode]
-    n_cols = 1
-    cols = np.zeros(t.nnz, dtype=np.int64)
-    for n in range(t.order):
-        if n == mode:
-            continue
-        cols = cols * t.shape[n] + coords[n]
-        n_cols *= t.shape[n]
+    others = [n for n in range(t.order) if n != mode]
+    n_cols = math.prod(t.shape[n] for n in others)
     k = min(rank, n_rows - 1, n_cols - 1)
     if k < 1:
         return g.random((n_rows, rank)) * scale
-    mat = csr_matrix((t.values, (rows, cols)), shape=(n_rows, n_cols))
-    u = svds(mat, k=k, return_singular_vectors="u", random_state=np.random.RandomState(0))[0]
+    cols = np.zeros(t.nnz, dtype=np.int64)
+    for n in others:                       # column = row-major key of the other modes
+        cols = cols * t.shape[n] + coords[n]
+    unfolding = csr_matrix((t.values, (coords[mode], cols)), shape=(n_rows, n_cols))
+    u = svds(unfolding, k=k, return_singular_vectors="u",
+             random_state=np.random.RandomState(0))[0]
     out = np.empty((n_rows, rank))
-    out[:, :k] = u[:, ::-1]
+    out[:, :k] = u[:, ::-1]                # svds returns ascending singular values
     if k < rank:
         out[:, k:] = g.random((n_rows, rank - k)) * scale
     return np.ascontiguousarray(out)
@@ -721,81 +727,94 @@ def sgd_sweep(t: SparseTensor, state: CompletionState, loss: LossFunction,
 # ---------------------------------------------------------------------------
 # orchestration
 
+def _one_iteration(t, state, loss, cfg, it: int, sgd_rng: RngState) -> None:
+    """One outer iteration of the configured algorithm (optim.py:655-664)."""
+    algo = cfg.algorithm
+    if algo == "sgd":
+        sgd_sweep(t, state, loss, cfg, sgd_rng.child(it))   # fresh sample stream per step
+    elif algo in ("gn", "newton"):
+        gn_step(t, state, loss, cfg, variant="gauss_newton" if algo == "gn" else "newton")
+    else:
+        {"als": als_sweep, "ccd": ccd_sweep}[algo](t, state, loss, cfg)
+    state.iteration = it
+
+
+def _require_finite_factors(factors, it: int) -> None:
+    # a NaN / inf anywhere in a factor makes its sum non-finite: one reduction
+    # per factor on whichever side (device or host) it lives
+    for d, f in enumerate(factors):
+        total = float(f.sum()) if _is_torch(f) else float(np.sum(f))
+        if not np.isfinite(total):
+            raise NumericalError(f"factor {d} became non-finite at iteration {it}; "
+                                 "reduce the step size or increase reg")
+
+
 def run(t: SparseTensor, cfg: SolverConfig, return_state: bool = False):
-    """Run the configured solver and collect a convergence trace (optim.py:604-691)."""
+    """Run the configured solver and collect a convergence trace.
+
+    Same contract as the reference's ``run`` (optim.py:604-691): record 0 is the
+    initial point; a record every ``record_every`` iterations (default 20 for
+    SGD, else 1) and at the last one; stop when the relative objective change
+    between records drops below ``tol``; NumericalError on non-finite factors
+    or a diverged objective.  Built-in losses keep the factors on the device
+    for the whole run and evaluate the objective there."""
     loss = get_loss(cfg.loss)
     loss.validate_data(t.values)
     root = RngState(cfg.seed)
     state = init_state(t, cfg, root.child(0))
     sgd_rng = root.child(1)
-    record_every = cfg.record_every
-    if record_every is None:
-        record_every = 20 if cfg.algorithm == "sgd" else 1
+    every = cfg.record_every if cfg.record_every is not None else (
+        20 if cfg.algorithm == "sgd" else 1)
+    is_ls = loss.ident == "ls"
     trace = RunTrace(
-        metric_name="rmse" if loss.ident == "ls" else "norm_loss",
+        metric_name="rmse" if is_ls else "norm_loss",
         metadata={"algorithm": cfg.algorithm, "loss": cfg.loss, "rank": str(cfg.rank),
                   "reg": repr(cfg.reg), "seed": str(cfg.seed),
-                  "shape": "x".join(str(d) for d in t.shape), "nnz": str(t.nnz)},
+                  "shape": "x".join(map(str, t.shape)), "nnz": str(t.nnz)},
     )
-    ls = loss.ident == "ls"
     on_device = loss.device_id is not None
     if on_device:
         state.factors = _to_dev_factors(state.factors)
     mask = t.observation_mask()
-    start = time.perf_counter()
-    if cfg.algorithm in ("gn", "newton") and cfg.warmup_sweeps:
-        for _ in range(cfg.warmup_sweeps):
-            als_sweep(t, state, loss, cfg)
+    count = max(t.nnz, 1)
+    t_start = time.perf_counter()
 
-    def evaluate():
-        if ls:
-            data_term = ls_data_term(t, state.factors)
-            obj = data_term + cfg.reg * factor_sq_norms(state.factors)
-            metric = float(np.sqrt(data_term / max(t.nnz, 1)))
-            return obj, metric
-        model = model_at_observed(mask, state.factors, threads=cfg.threads)
-        data_term = phi_sum(loss, t, model)
-        obj = data_term + cfg.reg * factor_sq_norms(state.factors)
-        return obj, data_term / max(t.nnz, 1)
-
-    def elapsed():
-        if cfg.deterministic:
+    def seconds() -> float:
+        if cfg.deterministic:       # byte-stable traces
             return 0.0
         _torch().cuda.synchronize()
-        return time.perf_counter() - start
+        return time.perf_counter() - t_start
 
-    obj, metric = evaluate()
-    trace.append(0, elapsed(), obj, metric)
-    initial_obj = obj
-    prev_obj = obj
-    for it in range(1, cfg.max_iters + 1):
-        if cfg.algorithm == "als":
-            als_sweep(t, state, loss, cfg)
-        elif cfg.algorithm == "ccd":
-            ccd_sweep(t, state, loss, cfg)
-        elif cfg.algorithm == "sgd":
-            sgd_sweep(t, state, loss, cfg, sgd_rng.child(it))
-        elif cfg.algorithm == "gn":
-            gn_step(t, state, loss, cfg, variant="gauss_newton")
+    def evaluate():
+        """(objective, metric): data term + reg * ||factors||^2, and rmse (least
+        squares) or the mean loss."""
+        if is_ls:
+            data = ls_data_term(t, state.factors)
+            metric = float(np.sqrt(data / count))
         else:
-            gn_step(t, state, loss, cfg, variant="newton")
-        state.iteration = it
-        for d, f in enumerate(state.factors):
-            total = float(f.sum()) if _is_torch(f) else float(np.sum(f))
-            if not np.isfinite(total):
-                raise NumericalError(f"factor {d} became non-finite at iteration {it}; "
-                                     "reduce the step size or increase reg")
-        if it % record_every == 0 or it == cfg.max_iters:
-            obj, metric = evaluate()
-            trace.append(it, elapsed(), obj, metric)
-            if not math.isfinite(obj) or obj > 1e3 * max(abs(initial_obj), 1.0):
-                raise NumericalError(f"objective diverged at iteration {it}: {obj!r} from "
-                                     f"{initial_obj!r}; reduce the step size or increase reg")
-            if abs(prev_obj - obj) / max(abs(prev_obj), _TINY) < cfg.tol:
-                break
-            prev_obj = obj
+            data = phi_sum(loss, t, model_at_observed(mask, state.factors, threads=cfg.threads))
+            metric = data / count
+        return data + cfg.reg * factor_sq_norms(state.factors), metric
+
+    if cfg.algorithm in ("gn", "newton"):
+        for _ in range(cfg.warmup_sweeps):
+            als_sweep(t, state, loss, cfg)
+    obj, metric = evaluate()
+    trace.append(0, seconds(), obj, metric)
+    first_obj = last_obj = obj
+    for it in range(1, cfg.max_iters + 1):
+        _one_iteration(t, state, loss, cfg, it, sgd_rng)
+        _require_finite_factors(state.factors, it)
+        if it % every and it != cfg.max_iters:
+            continue
+        obj, metric = evaluate()
+        trace.append(it, seconds(), obj, metric)
+        if not math.isfinite(obj) or obj > 1e3 * max(abs(first_obj), 1.0):
+            raise NumericalError(f"objective diverged at iteration {it}: {obj!r} from "
+                                 f"{first_obj!r}; reduce the step size or increase reg")
+        if abs(last_obj - obj) / max(abs(last_obj), _TINY) < cfg.tol:
+            break
+        last_obj = obj
     if on_device:
         state.factors = [f.double().cpu().numpy() for f in state.factors]
-    if return_state:
-        return trace, state
-    return trace
+    return (trace, state) if return_state else trace
