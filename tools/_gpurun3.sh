@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 200 python tools/cfg2_step.py 3 > gpurun_out/cfg2_step.log 2>&1 || exit 1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'tttp_kernel|mttkrp_kernel' -c 4 -o gpurun_out/r2s5_cfg2 -f python tools/cfg2_step.py 1 > gpurun_out/ncu_cfg2.log 2>&1
+timeout 300 python tools/sgd_one.py 1000000000 3 > gpurun_out/sgd_one.log 2>&1 || exit 1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/sgd_launches.csv python tools/sgd_one.py 1000000000 3 > gpurun_out/sgd_ncu.log 2>&1
