@@ -246,86 +246,155 @@ __global__ void offsets_from_sorted(const int32_t *__restrict__ sorted, int64_t 
 }
 
 // ---------------------------------------------------------------------------
-// stable LSD radix sort of (key, position) pairs by 8-bit digits
+// stable LSD radix sort of (key, position) pairs.  The digit width is chosen
+// per sort: the fewest passes with digits of at most RS_MAX_DIGIT bits, split
+// evenly (17 key bits -> 2 x 9 instead of 3 x 8; 10 -> 1 x 10; 40 -> 4 x 10).
 
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 8;
+constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
+#ifndef CPFIT_RS_MAX_DIGIT
+#define CPFIT_RS_MAX_DIGIT 10
+#endif
+constexpr int RS_MAX_DIGIT = CPFIT_RS_MAX_DIGIT;
 
 template <typename K>
-__device__ __forceinline__ int radix_digit(K key, int shift) {
-  return (int)((((typename std::make_unsigned<K>::type)key) >> shift) & 255u);
+__device__ __forceinline__ int radix_digit(K key, int shift, unsigned mask) {
+  return (int)((((typename std::make_unsigned<K>::type)key) >> shift) & mask);
 }
 
+// per-tile digit histogram -> counts[digit * nblocks + tile]
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS)
-radix_upsweep(const K *__restrict__ keys, int64_t n, int shift, int64_t nblocks,
+radix_upsweep(const K *__restrict__ keys, int64_t n, int shift, int nbins, int64_t nblocks,
               int32_t *__restrict__ counts) {
-  __shared__ int hist[256];
-  for (int i = threadIdx.x; i < 256; i += RS_THREADS) hist[i] = 0;
+  extern __shared__ int hist[];
+  const unsigned mask = (unsigned)nbins - 1u;
+  for (int i = threadIdx.x; i < nbins; i += RS_THREADS) hist[i] = 0;
   __syncthreads();
   int64_t base = (int64_t)blockIdx.x * RS_TILE;
   for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) {
     int64_t k = base + i;
-    if (k < n) atomicAdd(&hist[radix_digit(keys[k], shift)], 1);
+    if (k < n) atomicAdd(&hist[radix_digit(keys[k], shift, mask)], 1);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < 256; d += RS_THREADS)
+  for (int d = threadIdx.x; d < nbins; d += RS_THREADS)
     counts[(int64_t)d * nblocks + blockIdx.x] = hist[d];
 }
 
-// vals_in == nullptr means the identity (first pass).
+// vals_in == nullptr means the identity (first pass).  Ranks inside a tile
+// follow entry order (warp w's items before warp w+1's, item j before j+1,
+// lane order inside an item), so the sort is stable.  The tile is first
+// reordered by digit in shared memory, then written out position by position:
+// consecutive threads store consecutive addresses inside each digit's run
+// (whole 32-byte sectors instead of one 4-byte store per sector).
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS)
 radix_downsweep(const K *__restrict__ keys_in, const int32_t *__restrict__ vals_in,
-                int64_t n, int shift, int64_t nblocks, const int64_t *__restrict__ offs,
-                K *__restrict__ keys_out, int32_t *__restrict__ vals_out) {
-  __shared__ int whist[RS_WARPS][257];
+                int64_t n, int shift, int nbins, int64_t nblocks,
+                const int64_t *__restrict__ offs, K *__restrict__ keys_out,
+                int32_t *__restrict__ vals_out) {
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  // layout: staged keys [RS_TILE] | staged vals [RS_TILE] | digit starts [nbins + 1]
+  //         | per-warp histograms RS_WARPS x (nbins + 1)
+  K *skey = reinterpret_cast<K *>(rs_smem);
+  int32_t *sval = reinterpret_cast<int32_t *>(skey + RS_TILE);
+  int *dstart = reinterpret_cast<int *>(sval + RS_TILE);
+  int *whist_all = dstart + (nbins + 1);
+  __shared__ int wsum[RS_WARPS];
+  const int pitch = nbins + 1;
+  const unsigned mask = (unsigned)nbins - 1u;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int i = lane; i < 257; i += 32) whist[w][i] = 0;
+  int *whist = whist_all + w * pitch;
+  for (int i = lane; i < pitch; i += 32) whist[i] = 0;
   __syncwarp();
-  const int64_t wbase = (int64_t)blockIdx.x * RS_TILE + (int64_t)w * 32 * RS_ITEMS;
+  const int64_t tbase = (int64_t)blockIdx.x * RS_TILE;
+  const int64_t wbase = tbase + (int64_t)w * 32 * RS_ITEMS;
   K key[RS_ITEMS];
+  int32_t val[RS_ITEMS];
   int32_t rank[RS_ITEMS];
-  int digit[RS_ITEMS];
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
     int64_t k = wbase + j * 32 + lane;
     bool valid = k < n;
     key[j] = valid ? keys_in[k] : 0;
-    int d = valid ? radix_digit(key[j], shift) : 256;
-    digit[j] = d;
+    val[j] = valid ? (vals_in ? vals_in[k] : (int32_t)k) : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    int64_t k = wbase + j * 32 + lane;
+    int d = k < n ? radix_digit(key[j], shift, mask) : nbins;
     unsigned peers = __match_any_sync(0xffffffffu, d);
-    int pre = whist[w][d];
+    int pre = whist[d];
     __syncwarp();
     int leader = __ffs(peers) - 1;
-    if (lane == leader) whist[w][d] = pre + __popc(peers);
+    if (lane == leader) whist[d] = pre + __popc(peers);
     __syncwarp();
     rank[j] = pre + __popc(peers & lt);
   }
   __syncthreads();
-  // exclusive scan over warps per digit
-  for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
+  // per digit: exclusive scan over warps; the digit's tile total goes to dstart
+  for (int d = threadIdx.x; d < nbins; d += RS_THREADS) {
     int run = 0;
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ++ww) {
-      int c = whist[ww][d];
-      whist[ww][d] = run;
+      int c = whist_all[ww * pitch + d];
+      whist_all[ww * pitch + d] = run;
       run += c;
     }
+    dstart[d] = run;
   }
   __syncthreads();
+  // exclusive scan of the digit totals over the block (thread t owns a
+  // contiguous group of nbins / RS_THREADS digits, at least one)
+  {
+    const int per = nbins >= RS_THREADS ? nbins / RS_THREADS : 1;
+    const int d0 = threadIdx.x * per;
+    int local = 0;
+    if (d0 < nbins)
+      for (int i = 0; i < per; ++i) local += dstart[d0 + i];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int up = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += up;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    int wbefore = 0;
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww)
+      if (ww < w) wbefore += wsum[ww];
+    int run = wbefore + incl - local;
+    if (d0 < nbins)
+      for (int i = 0; i < per; ++i) {
+        int c = dstart[d0 + i];
+        dstart[d0 + i] = run;
+        run += c;
+      }
+  }
+  __syncthreads();
+  // stage the tile in digit order
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
     int64_t k = wbase + j * 32 + lane;
     if (k < n) {
-      int d = digit[j];
-      int64_t pos = offs[(int64_t)d * nblocks + blockIdx.x] + whist[w][d] + rank[j];
-      keys_out[pos] = key[j];
-      vals_out[pos] = vals_in ? vals_in[k] : (int32_t)k;
+      int d = radix_digit(key[j], shift, mask);
+      int lp = dstart[d] + whist[d] + rank[j];
+      skey[lp] = key[j];
+      sval[lp] = val[j];
     }
+  }
+  __syncthreads();
+  const int cnt = (int)(n - tbase < RS_TILE ? n - tbase : RS_TILE);
+  for (int i = threadIdx.x; i < cnt; i += RS_THREADS) {
+    K kk = skey[i];
+    int d = radix_digit(kk, shift, mask);
+    int64_t pos = offs[(int64_t)d * nblocks + blockIdx.x] + (i - dstart[d]);
+    keys_out[pos] = kk;
+    vals_out[pos] = sval[i];
   }
 }
 
@@ -335,7 +404,7 @@ radix_downsweep(const K *__restrict__ keys_in, const int32_t *__restrict__ vals_
 template <typename K>
 int radix_sort_pairs(const K *keys, int64_t n, int bits, K *sorted_keys, int32_t *perm,
                      cudaStream_t s) {
-  int passes = (bits + 7) / 8;
+  const int passes = (bits + RS_MAX_DIGIT - 1) / RS_MAX_DIGIT;
   if (passes == 0 || n <= 1) {
     iota_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(perm, n);
     CPFIT_LAUNCH_CHECK("iota");
@@ -343,12 +412,26 @@ int radix_sort_pairs(const K *keys, int64_t n, int bits, K *sorted_keys, int32_t
                                       cudaMemcpyDeviceToDevice, s));
     return CPFIT_OK;
   }
+  const int dbits = (bits + passes - 1) / passes;  // even split, <= RS_MAX_DIGIT
+  const int nbins = 1 << dbits;
+  const size_t up_smem = (size_t)nbins * sizeof(int);
+  const size_t down_smem = (size_t)RS_TILE * (sizeof(K) + sizeof(int32_t)) +
+                           (size_t)(RS_WARPS + 1) * (nbins + 1) * sizeof(int);
+  static bool attr_set = false;  // > 48 KB of dynamic shared memory needs the opt-in
+  if (!attr_set) {
+    constexpr size_t worst = (size_t)RS_TILE * (sizeof(K) + sizeof(int32_t)) +
+                             (size_t)(RS_WARPS + 1) * ((1 << RS_MAX_DIGIT) + 1) * sizeof(int);
+    static_assert(worst <= 200 * 1024, "radix tile does not fit shared memory");
+    CPFIT_CUDA(cudaFuncSetAttribute(radix_downsweep<K>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)worst));
+    attr_set = true;
+  }
   int64_t nblocks = (n + RS_TILE - 1) / RS_TILE;
   Scratch<int32_t> counts(s), v_tmp(s);
   Scratch<K> k_tmp(s);
   Scratch<int64_t> offs(s);
-  CPFIT_TRY(counts.alloc(256 * nblocks));
-  CPFIT_TRY(offs.alloc(256 * nblocks + 1));
+  CPFIT_TRY(counts.alloc((int64_t)nbins * nblocks));
+  CPFIT_TRY(offs.alloc((int64_t)nbins * nblocks + 1));
   CPFIT_TRY(k_tmp.alloc(n));
   CPFIT_TRY(v_tmp.alloc(n));
   // ping-pong so that the last pass lands in (sorted_keys, perm)
@@ -362,15 +445,15 @@ int radix_sort_pairs(const K *keys, int64_t n, int bits, K *sorted_keys, int32_t
   const K *kin = keys;
   const int32_t *vin = nullptr;
   for (int p = 0; p < passes; ++p) {
-    int shift = 8 * p;
-    radix_upsweep<K><<<(unsigned)nblocks, RS_THREADS, 0, s>>>(kin, n, shift, nblocks,
-                                                              counts.ptr);
+    int shift = dbits * p;
+    radix_upsweep<K><<<(unsigned)nblocks, RS_THREADS, up_smem, s>>>(kin, n, shift, nbins,
+                                                                     nblocks, counts.ptr);
     CPFIT_LAUNCH_CHECK("radix_upsweep");
-    CPFIT_TRY(exclusive_scan<int32_t>(counts.ptr, offs.ptr, 256 * nblocks, s));
+    CPFIT_TRY(exclusive_scan<int32_t>(counts.ptr, offs.ptr, (int64_t)nbins * nblocks, s));
     K *ko = kb[p % 2];
     int32_t *vo = vb[p % 2];
-    radix_downsweep<K><<<(unsigned)nblocks, RS_THREADS, 0, s>>>(kin, vin, n, shift, nblocks,
-                                                                offs.ptr, ko, vo);
+    radix_downsweep<K><<<(unsigned)nblocks, RS_THREADS, down_smem, s>>>(
+        kin, vin, n, shift, nbins, nblocks, offs.ptr, ko, vo);
     CPFIT_LAUNCH_CHECK("radix_downsweep");
     kin = ko;
     vin = vo;
