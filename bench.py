@@ -774,7 +774,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-ref", action="store_true",
                     help="skip the on-box CPU reference legs of the cfg 3/4/5 sections")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-als", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-sgd", action="store_true")
