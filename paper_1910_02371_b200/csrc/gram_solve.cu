@@ -270,8 +270,15 @@ gram_kernel(const GramParams<T> p) {
 // work.  Tile set as gram_kernel (upper-triangular 8x8 tiles); the per-tile
 // accumulation order over k is the same, so results agree with gram_kernel
 // to rounding of the (identical) products.
+// k-steps (of 4 entries) per stage and the stage schedule.  Measured at cfg 3
+// (ALS sweep, ms): ping-pong buffers U=2 22.96 (round-2 default until session
+// 5); ORDER 1 U=2 22.44, U=3 21.02, U=4 (202 registers) 22.5; ORDER 2 U=3
+// 22.6; ORDER 3 U=3 22.3 (profiles/r2_tuning.md).
 #ifndef CPFIT_GRAM_FRAG_U
-#define CPFIT_GRAM_FRAG_U 2
+#define CPFIT_GRAM_FRAG_U 3
+#endif
+#ifndef CPFIT_GRAM_ORDER
+#define CPFIT_GRAM_ORDER 1
 #endif
 constexpr int GRAM_FRAG_WARPS = 4;
 
@@ -374,32 +381,6 @@ gram_frag_kernel(const GramParams<double> p) {
 #pragma unroll
     for (int i = 0; i < RT; ++i) racc[i] = 0.0;
     int32_t ix_next[U][NPT];
-    // two stage buffers used alternately (no register copies between stages)
-    GramFragStage<RT, NPT, U> sa, sb;
-    auto mma_stage = [&](const GramFragStage<RT, NPT, U> &st, int64_t kb) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        double f[RT];
-#pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          double prod = st.x[u][0][i];
-#pragma unroll
-          for (int n = 1; n < NPT; ++n) prod *= st.x[u][n][i];
-          f[i] = prod * st.sw[u];
-          racc[i] = fma(st.tv[u], prod, racc[i]);
-        }
-        if (kb + 4 * u < b1) {
-          int tile = 0;
-#pragma unroll
-          for (int i = 0; i < RT; ++i)
-#pragma unroll
-            for (int jt = i; jt < RT; ++jt) {
-              dmma_8x8x4(acc[tile][0], acc[tile][1], f[i], f[jt]);
-              ++tile;
-            }
-        }
-      }
-    };
     // stage loaders: the predicate-free variants when the whole stage lies
     // inside the task (warp-uniform test), the generic ones at the tail
     auto load_idx = [&](int64_t ks, int32_t(&ix)[U][NPT]) {
@@ -410,25 +391,113 @@ gram_frag_kernel(const GramParams<double> p) {
       if (FULLR && ks + KS <= b1) gram_frag_load_full<RT, NPT, U, WEIGHTED, RHS>(p, ks, gq, tq, ix, st);
       else gram_frag_load<RT, NPT, U>(p, ks, b1, gq, tq, ix, st);
     };
+    // Hadamard rows of a stage -> MMA operands f (and the fused rhs)
+    auto hadamard = [&](const GramFragStage<RT, NPT, U> &st, double (&f)[U][RT]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          double prod = st.x[u][0][i];
+#pragma unroll
+          for (int n = 1; n < NPT; ++n) prod *= st.x[u][n][i];
+          f[u][i] = prod * st.sw[u];
+          racc[i] = fma(st.tv[u], prod, racc[i]);
+        }
+    };
+    auto dmma_stage = [&](const double (&f)[U][RT], int64_t kb) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (kb + 4 * u < b1) {
+          int tile = 0;
+#pragma unroll
+          for (int i = 0; i < RT; ++i)
+#pragma unroll
+            for (int jt = i; jt < RT; ++jt) {
+              dmma_8x8x4(acc[tile][0], acc[tile][1], f[u][i], f[u][jt]);
+              ++tile;
+            }
+        }
+    };
+#if CPFIT_GRAM_ORDER == 1
+    // One stage buffer.  A stage is first consumed into its MMA operands (the
+    // only wait on gathered rows, with nothing younger in flight), THEN the
+    // next stage's gathers and the indices after it are issued into the same
+    // registers, then the MMAs run under them.  In the ping-pong order below
+    // ptxas put the freshly issued stream / gather loads on the scoreboard the
+    // first Hadamard multiply waits on in one of the two loop copies (ncu:
+    // 26 % of the kernel's samples on that DMUL against 3 % in the other copy).
+    GramFragStage<RT, NPT, U> sa;
     {
       int32_t ix0[U][NPT];
       load_idx(b0, ix0);
       load_idx(b0 + KS, ix_next);
       load_rows(b0, ix0, sa);
     }
+    for (int64_t kb = b0; kb < b1; kb += KS) {
+      double f[U][RT];
+      hadamard(sa, f);
+      load_rows(kb + KS, ix_next, sa);
+      load_idx(kb + 2 * KS, ix_next);
+      dmma_stage(f, kb);
+    }
+#elif CPFIT_GRAM_ORDER == 2
+    // no overlap inside a warp: operands, MMAs, then the next stage's loads
+    GramFragStage<RT, NPT, U> sa;
+    {
+      int32_t ix0[U][NPT];
+      load_idx(b0, ix0);
+      load_idx(b0 + KS, ix_next);
+      load_rows(b0, ix0, sa);
+    }
+    for (int64_t kb = b0; kb < b1; kb += KS) {
+      double f[U][RT];
+      hadamard(sa, f);
+      dmma_stage(f, kb);
+      load_rows(kb + KS, ix_next, sa);
+      load_idx(kb + 2 * KS, ix_next);
+    }
+#elif CPFIT_GRAM_ORDER == 3
+    // as 1, the index stream loads after the MMAs
+    GramFragStage<RT, NPT, U> sa;
+    {
+      int32_t ix0[U][NPT];
+      load_idx(b0, ix0);
+      load_idx(b0 + KS, ix_next);
+      load_rows(b0, ix0, sa);
+    }
+    for (int64_t kb = b0; kb < b1; kb += KS) {
+      double f[U][RT];
+      hadamard(sa, f);
+      load_rows(kb + KS, ix_next, sa);
+      dmma_stage(f, kb);
+      load_idx(kb + 2 * KS, ix_next);
+    }
+#else
+    // two stage buffers used alternately (no register copies between stages):
     // the next stage's gathers (indices loaded one stage earlier) and the
     // indices of the stage after it are issued before this stage's MMAs
+    GramFragStage<RT, NPT, U> sa, sb;
+    {
+      int32_t ix0[U][NPT];
+      load_idx(b0, ix0);
+      load_idx(b0 + KS, ix_next);
+      load_rows(b0, ix0, sa);
+    }
     for (int64_t kb = b0; kb < b1;) {
+      double f[U][RT];
       load_rows(kb + KS, ix_next, sb);
       load_idx(kb + 2 * KS, ix_next);
-      mma_stage(sa, kb);
+      hadamard(sa, f);
+      dmma_stage(f, kb);
       kb += KS;
       if (kb >= b1) break;
       load_rows(kb + KS, ix_next, sa);
       load_idx(kb + 2 * KS, ix_next);
-      mma_stage(sb, kb);
+      hadamard(sb, f);
+      dmma_stage(f, kb);
       kb += KS;
     }
+#endif
     const int slot = p.task_slot[t];
     double *dst = slot < 0 ? p.gram + (int64_t)p.task_row[t] * rank * rank
                            : p.partial + (int64_t)slot * p.pstride;
