@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ccd_launches.csv python tools/ccd_profile.py 100480507 4 > gpurun_out/ncu_ccd2.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'solve_reg_kernel' --launch-skip 3 -c 1 -o gpurun_out/r2s5_solve -f python tools/als_sweep_once.py > gpurun_out/ncu_solve.log 2>&1
