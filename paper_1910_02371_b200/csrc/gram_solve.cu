@@ -543,11 +543,26 @@ __global__ void combine_gram_partials(const int32_t *__restrict__ split_row,
   for (int64_t s = blockIdx.x; s < nsplit; s += gridDim.x) {
     const int64_t row = split_row[s];
     const int64_t a = split_slot[s], b = split_slot[s + 1];
-    for (int64_t c = threadIdx.x; c < pstride; c += blockDim.x) {
-      double acc = (double)partial[a * pstride + c];
-      for (int64_t k = a + 1; k < b; ++k) acc += (double)partial[k * pstride + c];
-      if (c < rr) gram[row * rr + c] = (T)acc;
-      else rhs[row * rank + (c - rr)] = (T)acc;
+    // columns are spread over gridDim.y blocks so that a long row is not one block's work
+    for (int64_t c = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; c < pstride;
+         c += (int64_t)gridDim.y * blockDim.x) {
+      // eight interleaved running sums (slot k -> sum k mod 8), added by a fixed
+      // tree: a Zipf head row has ~1000 partial blocks, and one running sum made
+      // every thread wait for 1000 dependent loads (cfg 3 mode 1: 0.54 ms)
+      double acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+      int64_t k = a;
+      for (; k + 8 <= b; k += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += (double)partial[(k + j) * pstride + c];
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (k + j < b) acc[j] += (double)partial[(k + j) * pstride + c];
+      const double tot = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      if (c < rr) gram[row * rr + c] = (T)tot;
+      else rhs[row * rank + (c - rr)] = (T)tot;
     }
   }
 }
@@ -778,7 +793,8 @@ static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
   }
   CPFIT_TRY(launch_gram<T>(p, s));
   if (L.nsplit > 0) {
-    unsigned grid = (unsigned)(L.nsplit < 65535 ? L.nsplit : 65535);
+    dim3 grid((unsigned)(L.nsplit < 65535 ? L.nsplit : 65535),
+              (unsigned)((p.pstride + 255) / 256));
     combine_gram_partials<T><<<grid, 256, 0, s>>>(L.split_row, L.split_slot, L.nsplit, rr,
                                                   p.pstride, partial.ptr, gram, rhs, rank);
     CPFIT_LAUNCH_CHECK("combine_gram_partials");

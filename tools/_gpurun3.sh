@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'solve_reg_kernel' --launch-skip 3 -c 1 -o gpurun_out/r2s5_solve -f python tools/als_sweep_once.py > gpurun_out/ncu_solve.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gputest.log 2>&1; echo "pytest exit $?" >> gpurun_out/gputest.log
+timeout 300 python tools/als_modes.py 100480507 > gpurun_out/als_modes.log 2>&1
