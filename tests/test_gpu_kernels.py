@@ -371,3 +371,46 @@ def test_nonfinite_factors_raise_like_reference():
         cp.tttp(t, [good, good, np.ones((3, 3))])
     # valid calls still work after a rejected one
     assert cp.tttp(t, [good, good, good]).values.tolist() == [3.0, 6.0]
+
+
+@pytest.mark.parametrize("dim1,nnz", [
+    (2, 1), (2, 4095), (3, 4096), (300, 4097), (513, 8192), (1024, 12289),
+    (1025, 20000), (70000, 50000), (300000, 70001), (1 << 20, 33000), ((1 << 20) + 1, 33000),
+])
+def test_mode_sort_digit_widths_and_tile_edges(dim1, nnz):
+    """The stable LSD radix sort behind counting_sort_by_mode (core.py:234-249)
+    chooses its digit width per sort and works on 4096-entry tiles: key widths of
+    1 ... 21 bits (1, 2 and 3 passes, even and uneven digit splits) at entry counts
+    on and next to tile edges; permutation and offsets bit-identical to numpy's
+    stable argsort.  The mode-1 keys are heavily repeated (stability matters)."""
+    rng = np.random.default_rng(dim1 * 7919 + nnz)
+    dims = (max(2, (4 * nnz) // dim1 + 2), dim1, 5)
+    total = int(np.prod([int(d) for d in dims], dtype=object))
+    keys = np.unique(rng.integers(0, total, size=int(nnz * 1.3), dtype=np.int64))
+    keys = np.sort(rng.choice(keys, size=min(nnz, keys.size), replace=False)).astype(np.uint64)
+    t = cp.SparseTensor(dims, keys, np.ones(keys.size))
+    coords = cp.delinearize_many(keys, dims)
+    for mode in range(3):
+        perm, offsets = t.mode_group(mode)
+        want = np.argsort(coords[mode], kind="stable")
+        assert np.array_equal(np.asarray(perm, dtype=np.int64), want), (mode, dims)
+        counts = np.bincount(coords[mode], minlength=dims[mode])
+        assert np.array_equal(np.asarray(offsets), np.concatenate(([0], np.cumsum(counts))))
+
+
+def test_from_coords_wide_keys_sort():
+    """Ingest sort of 60-bit linearized keys (6 passes of 10-bit digits) with
+    duplicates: keys and merged values equal numpy's (core.py:208-231)."""
+    rng = np.random.default_rng(3)
+    dims = (1 << 20, 1 << 20, 1 << 20)
+    n = 30000
+    c = [rng.integers(0, d, n) for d in dims]
+    for k in range(3):          # force duplicates
+        c[k][n // 2:] = c[k][: n - n // 2]
+    v = rng.standard_normal(n)
+    t = cp.from_coords(c, v, dims)
+    keys = cp.linearize_many(c, dims)
+    order = np.argsort(keys, kind="stable")
+    uk, start = np.unique(keys[order], return_index=True)
+    assert np.array_equal(t.keys, uk)
+    np.testing.assert_allclose(t.values, np.add.reduceat(v[order], start), rtol=0, atol=0)
