@@ -91,15 +91,36 @@ static int run_tttp_host(cpfit_pattern *pt, int rank, const void *vals,
   return CPFIT_OK;
 }
 
+// rows of the target mode without entries -> exact zeros (warp per row)
+template <typename T>
+__global__ void mttkrp_zero_empty_rows(int64_t dim, const int64_t *__restrict__ offsets, int rank,
+                                       T *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < dim; i += nwarps) {
+    if (offsets[i + 1] != offsets[i]) continue;
+    for (int c = lane; c < rank; c += 32) out[i * rank + c] = T(0);
+  }
+}
+
 template <typename T>
 static int run_mttkrp(cpfit_pattern *pt, int mode, int rank, const void *vals, int vals_sorted,
                       const void *const *factors, void *out, cudaStream_t s,
                       const void *xvec = nullptr, const int32_t *row_active = nullptr) {
   const int64_t dim = pt->dims[mode];
-  CPFIT_CUDA(cudaMemsetAsync(out, 0, (size_t)dim * rank * sizeof(T), s));
-  if (pt->nnz == 0) return CPFIT_OK;
+  if (pt->nnz == 0) {
+    CPFIT_CUDA(cudaMemsetAsync(out, 0, (size_t)dim * rank * sizeof(T), s));
+    return CPFIT_OK;
+  }
   CPFIT_TRY(ensure_layout(pt, mode, s));
   CpfitModeLayout &L = pt->modes[mode];
+  // every non-empty row is stored by its task (or by the combine of its split
+  // tasks), so only the rows without entries are zeroed: `out` is written
+  // exactly once, which also lets it be pinned host memory (the numpy API
+  // passes its result buffer, no separate read-back pass)
+  mttkrp_zero_empty_rows<T><<<grid_for(dim * 32, 256), 256, 0, s>>>(dim, L.offsets, rank, (T *)out);
+  CPFIT_LAUNCH_CHECK("mttkrp_zero_empty_rows");
   MttkrpParams<T> p{};
   p.rank = rank;
   int np = 0;

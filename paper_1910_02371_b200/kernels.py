@@ -19,6 +19,8 @@ results are thread-count independent too (kernels.py:12-15).
 
 from __future__ import annotations
 
+import os
+
 import ctypes
 
 import numpy as np
@@ -132,6 +134,9 @@ def _stream():
 
 # ---------------------------------------------------------------------------
 
+_MTTKRP_DIRECT_HOST = os.environ.get("CPFIT_MTTKRP_DIRECT_HOST", "1") != "0"
+
+
 def mttkrp(t: SparseTensor, factors, mode: int, threads: int = 1):
     """Matricized tensor times Khatri-Rao product (kernels.py:46-91).
 
@@ -145,7 +150,13 @@ def mttkrp(t: SparseTensor, factors, mode: int, threads: int = 1):
     torch = _torch()
     dev = [_to_device(f, dtype) for f in factors]
     fin = _FiniteCheck(_named(factors, dev))
-    out = torch.empty((t.shape[mode], rank), dtype=dtype, device=cuda_device())
+    if on_device or not _MTTKRP_DIRECT_HOST:
+        out = torch.empty((t.shape[mode], rank), dtype=dtype, device=cuda_device())
+    else:
+        # numpy operands: the kernel stores its rows straight into the pinned
+        # result buffer (each row is written once, 128-byte aligned stores), so
+        # the result needs no read-back pass behind whatever else is crossing PCIe
+        out = torch.empty((t.shape[mode], rank), dtype=dtype, pin_memory=True)
     if t.nnz == 0:
         out.zero_()
     else:
@@ -153,7 +164,13 @@ def mttkrp(t: SparseTensor, factors, mode: int, threads: int = 1):
         _lib.check(_lib.load().cpfit_mttkrp(
             t.device_pattern().handle, mode, _dtype_code(dtype), rank, _vp(vals), 1,
             _ptrs(dev), _vp(out), _stream()), "mttkrp")
-    res = out if on_device else to_host_sm(out)
+    if on_device:
+        res = out
+    elif _MTTKRP_DIRECT_HOST:
+        torch.cuda.current_stream().synchronize()
+        res = out.numpy()
+    else:
+        res = to_host_sm(out)
     fin.raise_if_bad()
     return res
 
