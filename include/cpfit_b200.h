@@ -120,6 +120,9 @@ int cpfit_tttp(cpfit_pattern *p, int dtype, int rank, const void *vals,
  *                       factors[k][i_k(e), r];  rows without entries are 0.
  * `vals_sorted` != 0 means `vals` is already in the mode-sorted order
  * (cpfit_permute_values), otherwise it is in canonical order.
+ * Every element of `out` is stored exactly once (no zero fill followed by
+ * accumulation), so `out` may be device memory or device-accessible pinned
+ * host memory (the numpy binding passes its result buffer).
  * Replaces: kernels.mttkrp (kernels.py:46-91), _jit.mttkrp3 (_jit.py:35-47). */
 int cpfit_mttkrp(cpfit_pattern *p, int mode, int dtype, int rank,
                  const void *vals, int vals_sorted,
