@@ -270,10 +270,11 @@ gram_kernel(const GramParams<T> p) {
 // work.  Tile set as gram_kernel (upper-triangular 8x8 tiles); the per-tile
 // accumulation order over k is the same, so results agree with gram_kernel
 // to rounding of the (identical) products.
-// k-steps (of 4 entries) per stage and the stage schedule.  Measured at cfg 3
-// (ALS sweep, ms): ping-pong buffers U=2 22.96 (round-2 default until session
-// 5); ORDER 1 U=2 22.44, U=3 21.02, U=4 (202 registers) 22.5; ORDER 2 U=3
-// 22.6; ORDER 3 U=3 22.3 (profiles/r2_tuning.md).
+// k-steps (of 4 entries) per stage and the stage schedule (1: one buffer,
+// operands before the next loads; 0: the earlier ping-pong buffers).  Measured at
+// cfg 3 (ALS sweep, ms): ping-pong U=2 22.96; one buffer U=2 22.44, U=3 21.02,
+// U=4 (202 registers) 22.5; schedules without intra-warp overlap or with the
+// index loads after the MMAs 22.3-22.6 (profiles/r2_tuning.md).
 #ifndef CPFIT_GRAM_FRAG_U
 #define CPFIT_GRAM_FRAG_U 3
 #endif
@@ -439,38 +440,6 @@ gram_frag_kernel(const GramParams<double> p) {
       load_rows(kb + KS, ix_next, sa);
       load_idx(kb + 2 * KS, ix_next);
       dmma_stage(f, kb);
-    }
-#elif CPFIT_GRAM_ORDER == 2
-    // no overlap inside a warp: operands, MMAs, then the next stage's loads
-    GramFragStage<RT, NPT, U> sa;
-    {
-      int32_t ix0[U][NPT];
-      load_idx(b0, ix0);
-      load_idx(b0 + KS, ix_next);
-      load_rows(b0, ix0, sa);
-    }
-    for (int64_t kb = b0; kb < b1; kb += KS) {
-      double f[U][RT];
-      hadamard(sa, f);
-      dmma_stage(f, kb);
-      load_rows(kb + KS, ix_next, sa);
-      load_idx(kb + 2 * KS, ix_next);
-    }
-#elif CPFIT_GRAM_ORDER == 3
-    // as 1, the index stream loads after the MMAs
-    GramFragStage<RT, NPT, U> sa;
-    {
-      int32_t ix0[U][NPT];
-      load_idx(b0, ix0);
-      load_idx(b0 + KS, ix_next);
-      load_rows(b0, ix0, sa);
-    }
-    for (int64_t kb = b0; kb < b1; kb += KS) {
-      double f[U][RT];
-      hadamard(sa, f);
-      load_rows(kb + KS, ix_next, sa);
-      dmma_stage(f, kb);
-      load_idx(kb + 2 * KS, ix_next);
     }
 #else
     // two stage buffers used alternately (no register copies between stages):
