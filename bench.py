@@ -859,7 +859,8 @@ def main():
         nt, ns, nsl = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _lib.check(L.cpfit_pattern_mode_stats(pat.handle, m, sp, ctypes.byref(nt),
                                               ctypes.byref(ns), ctypes.byref(nsl)))
-        launches_per_step += 1 + (1 if ns.value > 0 else 0)
+        # mttkrp_zero_empty_rows + mttkrp_kernel (+ combine_partials when rows are split)
+        launches_per_step += 2 + (1 if ns.value > 0 else 0)
     F64 = _dtype_code(torch.float64)
     ev = {k: [] for k in ("tttp", "m0", "m1", "m2")}
 
