@@ -759,6 +759,9 @@ static int run_gram(cpfit_pattern *pt, int mode, int rank, const T *weights,
         pt->nnz, weights, p.wperm, sqw.ptr);
     CPFIT_LAUNCH_CHECK("sqrt_weights");
     p.sqrt_w = sqw.ptr;
+    // sqrt_w is in mode-sorted order and supersedes (weights, wperm): with the
+    // permutation cleared the predicate-free full-stage kernel is eligible
+    p.wperm = nullptr;
   }
   CPFIT_TRY(launch_gram<T>(p, s));
   if (L.nsplit > 0) {
